@@ -1,0 +1,107 @@
+/*
+ * fraclap_b200 — C ABI of the B200-native hot path of the fractional-Laplacian
+ * optimal-control solver (arXiv 1809.01971; reference package `fraclap`).
+ *
+ * Plain pointers and sizes only: every array argument is a DEVICE pointer to
+ * fp64 data (unless stated otherwise), every size is int64_t, `stream` is a
+ * cudaStream_t passed as void* (NULL = legacy default stream).  All entry
+ * points are asynchronous on `stream` unless marked "sync".
+ *
+ * Return value: FL_OK (0) on success; FL_EINVAL for an argument the
+ * reference would reject with ValueError; FL_ECUDA / FL_ENOMEM for device
+ * failures.  fl_last_error() returns the message of the last failure on the
+ * calling thread.
+ *
+ * Layout convention: a d-way full tensor with dims (n0, .., n_{d-1}) is
+ * C-ordered (last index fastest).  A canonical factor matrix U^(l) of shape
+ * (n_l, R) is row-major (R fastest), exactly the numpy layout of the
+ * reference's `CpTensor.factors` (tensor.py:54-96).
+ *
+ * Reference interface each entry point replaces is cited as file:line of
+ * /root/reference/pkg/src/fraclap/.
+ */
+#ifndef FRACLAP_B200_H
+#define FRACLAP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FL_OK 0
+#define FL_EINVAL 1
+#define FL_ECUDA 2
+#define FL_ENOMEM 3
+
+/* core function tags (fracop.py:58 _TAGS) */
+#define FL_G1 0 /* cm * rho^-a                 */
+#define FL_G2 1 /* cm * rho^-a + cp * rho^a    */
+#define FL_G3 2 /* 1 / g2                      */
+#define FL_G4 3 /* 1 / (1 + cp * rho^(2a))     */
+
+/* ---- library / device info ------------------------------------------ */
+int fl_version(void);
+const char* fl_last_error(void);
+int fl_sm_count(void);
+/* sync: build the per-n transform tables (twiddles, sine tables, dense sine
+ * matrices).  Called implicitly on first use; call it up front before CUDA
+ * graph capture. */
+int fl_prepare(int64_t n);
+
+/* ---- spectral: orthonormal DST-I --------------------------------------
+ * Replaces spectral.dst_apply (spectral.py:295-318, analytic-dst branch:
+ * scipy.fft.dst(x, type=1, norm="ortho", axis=0)) and its batched use in
+ * fracop.apply (fracop.py:490-493).
+ * Treats x as [outer][n][inner] and transforms the middle axis:
+ *   y[o][k][c] = scale * sqrt(2/(n+1)) * sum_j sin(pi (j+1)(k+1)/(n+1)) x[o][j][c]
+ * x == y (in place) is allowed.  n+1 a power of two in [4, 8192] runs the
+ * FFT kernel; any other n runs the dense sine-matrix kernel. */
+int fl_dst1(const double* x, double* y, int64_t outer, int64_t n, int64_t inner,
+            double scale, void* stream);
+
+/* Dense-eigenbasis transform (spectral.py:316-318 for generalized_mode):
+ * y[o] = Q^T x[o] (forward) or Q x[o] (inverse) along the middle axis, Q
+ * an (n, n) row-major orthonormal matrix on the device. */
+int fl_basis_apply(const double* Q, int transpose, const double* x, double* y,
+                   int64_t outer, int64_t n, int64_t inner, void* stream);
+
+/* ---- fracop: cores ------------------------------------------------------
+ * Dense core evaluation, fracop._dense_core / _eval_on_rho
+ * (fracop.py:109-148): out[i] = g(rho(i)), rho(i) = sum_l mu_l[i_l],
+ * with g selected by tag (FL_G1..FL_G4), outer exponent a, coefficients
+ * cm, cp, and `reciprocal` (1 -> 1/g).  mu: d device pointers (host array
+ * of pointers). */
+int fl_core_eval(double* out, int d, const int64_t* dims, const double* const* mu,
+                 int tag, double a, double cm, double cp, int reciprocal,
+                 void* stream);
+
+/* cp_to_dense (tensor.py:217-225): out[i] = sum_k w[k] prod_l U_l[i_l, k]. */
+int fl_cp_to_dense(double* out, int d, const int64_t* dims, int64_t rank,
+                   const double* weights, const double* const* factors,
+                   void* stream);
+
+/* Sinc-quadrature factors, fracop._sinc_core (fracop.py:194-199):
+ * U[i, k] = exp(-(mu[i] / rho_min) * t[k]) for an (n, R) row-major U. */
+int fl_sinc_factor(double* U, const double* mu, int64_t n, const double* t,
+                   int64_t R, double rho_min, void* stream);
+
+/* ---- full-format operator application ---------------------------------
+ * y = alpha * F diag(core) F x on a d-way tensor (d = 2 or 3), F the
+ * per-mode orthonormal DST-I (the full-format form of fracop.apply; the
+ * reference's dense oracle is tests/oracles.py:56 dense_apply).  `core` is
+ * a dense core tensor of the same dims (from fl_core_eval / fl_cp_to_dense).
+ * x == y allowed.  The last mode runs forward DST, core scaling and the
+ * inverse DST in one fused pass; the other modes one pass each way. */
+int fl_apply_full(const double* x, double* y, const double* core, int d,
+                  const int64_t* dims, double alpha, void* stream);
+
+/* y = alpha * F x over all d modes (a full spectral transform). */
+int fl_transform_full(const double* x, double* y, int d, const int64_t* dims,
+                      double alpha, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FRACLAP_B200_H */

@@ -1,0 +1,128 @@
+// extern "C" entry points of libfraclap_b200.so (see include/fraclap_b200.h).
+#include <cstdarg>
+#include <cstdio>
+#include <mutex>
+#include <map>
+#include <cmath>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace fl {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int sm_count() {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+  cache[dev] = v;
+  return v;
+}
+
+static int check_dims(int d, const int64_t* dims) {
+  FL_ARG_CHECK(d == 2 || d == 3, "only tensors of order 2 or 3 are supported, got %d", d);
+  for (int l = 0; l < d; ++l) FL_ARG_CHECK(dims[l] >= 1, "mode %d has size %lld", l, (long long)dims[l]);
+  return FL_OK;
+}
+
+}  // namespace fl
+
+using namespace fl;
+
+extern "C" {
+
+int fl_version(void) { return 1; }
+
+const char* fl_last_error(void) { return g_err; }
+
+int fl_sm_count(void) { return sm_count(); }
+
+int fl_prepare(int64_t n) { return prepare(n); }
+
+int fl_dst1(const double* x, double* y, int64_t outer, int64_t n, int64_t inner, double scale, void* stream) {
+  return dst_mode(x, y, outer, n, inner, scale, nullptr, as_stream(stream));
+}
+
+int fl_basis_apply(const double* Q, int transpose, const double* x, double* y, int64_t outer, int64_t n,
+                   int64_t inner, void* stream) {
+  FL_ARG_CHECK(n >= 1 && inner >= 1 && outer >= 0, "bad transform shape");
+  FL_ARG_CHECK(x != y, "fl_basis_apply does not run in place");
+  // forward (transpose=1): y = Q^T x ; inverse: y = Q x
+  const int64_t sAm = transpose ? 1 : n, sAk = transpose ? n : 1;
+  return gemm_f64(n, inner, n, 1.0, Q, sAm, sAk, 0, x, inner, 1, n * inner, 0.0, y, inner, 1, n * inner, outer,
+                  as_stream(stream));
+}
+
+int fl_core_eval(double* out, int d, const int64_t* dims, const double* const* mu, int tag, double a, double cm,
+                 double cp, int reciprocal, void* stream) {
+  int rc = check_dims(d, dims);
+  if (rc) return rc;
+  return core_eval(out, d, dims, mu, tag, a, cm, cp, reciprocal, as_stream(stream));
+}
+
+int fl_cp_to_dense(double* out, int d, const int64_t* dims, int64_t rank, const double* weights,
+                   const double* const* factors, void* stream) {
+  int rc = check_dims(d, dims);
+  if (rc) return rc;
+  FL_ARG_CHECK(rank >= 0, "rank must be nonnegative");
+  return cp_to_dense(out, d, dims, rank, weights, factors, as_stream(stream));
+}
+
+int fl_sinc_factor(double* U, const double* mu, int64_t n, const double* t, int64_t R, double rho_min,
+                   void* stream) {
+  FL_ARG_CHECK(n >= 1 && R >= 0, "bad sinc factor shape");
+  FL_ARG_CHECK(rho_min > 0.0, "rho_min must be positive");
+  return sinc_factor(U, mu, n, t, R, rho_min, as_stream(stream));
+}
+
+// y = alpha * F diag(core) F x, F = per-mode orthonormal DST-I.
+int fl_apply_full(const double* x, double* y, const double* core, int d, const int64_t* dims, double alpha,
+                  void* stream) {
+  int rc = check_dims(d, dims);
+  if (rc) return rc;
+  FL_ARG_CHECK(core != nullptr, "core tensor required");
+  cudaStream_t st = as_stream(stream);
+  if (d == 2) {
+    const int64_t n0 = dims[0], n1 = dims[1];
+    if ((rc = dst_mode(x, y, 1, n0, n1, 1.0, nullptr, st))) return rc;
+    if ((rc = dst_mode(y, y, n0, n1, 1, 1.0, core, st))) return rc;
+    return dst_mode(y, y, 1, n0, n1, alpha, nullptr, st);
+  }
+  const int64_t n0 = dims[0], n1 = dims[1], n2 = dims[2];
+  if ((rc = dst_mode(x, y, 1, n0, n1 * n2, 1.0, nullptr, st))) return rc;
+  if ((rc = dst_mode(y, y, n0, n1, n2, 1.0, nullptr, st))) return rc;
+  if ((rc = dst_mode(y, y, n0 * n1, n2, 1, 1.0, core, st))) return rc;
+  if ((rc = dst_mode(y, y, n0, n1, n2, 1.0, nullptr, st))) return rc;
+  return dst_mode(y, y, 1, n0, n1 * n2, alpha, nullptr, st);
+}
+
+int fl_transform_full(const double* x, double* y, int d, const int64_t* dims, double alpha, void* stream) {
+  int rc = check_dims(d, dims);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  if (d == 2) {
+    const int64_t n0 = dims[0], n1 = dims[1];
+    if ((rc = dst_mode(x, y, n0, n1, 1, 1.0, nullptr, st))) return rc;
+    return dst_mode(y, y, 1, n0, n1, alpha, nullptr, st);
+  }
+  const int64_t n0 = dims[0], n1 = dims[1], n2 = dims[2];
+  if ((rc = dst_mode(x, y, n0 * n1, n2, 1, 1.0, nullptr, st))) return rc;
+  if ((rc = dst_mode(y, y, n0, n1, n2, 1.0, nullptr, st))) return rc;
+  return dst_mode(y, y, 1, n0, n1 * n2, alpha, nullptr, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,285 @@
+// Host side of the DST-I transforms: per-length tables, kernel dispatch,
+// and the dense sine-matrix path for lengths without an FFT plan.
+#include <cmath>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+#include "dst_fft.cuh"
+#include "kernels.cuh"
+
+namespace fl {
+
+namespace {
+
+struct Tables {
+  double2* tw = nullptr;
+  double* sn = nullptr;
+  int* perm = nullptr;
+  double* sine = nullptr;  // dense n x n unnormalised sine matrix (non-FFT lengths)
+};
+
+std::mutex g_mu;
+std::map<std::pair<int, int64_t>, Tables> g_tables;  // (device, n)
+
+int ilog2_exact(int64_t v) {
+  if (v <= 0 || (v & (v - 1))) return -1;
+  int l = 0;
+  while ((int64_t(1) << l) < v) ++l;
+  return l;
+}
+
+bool fft_len_ok(int64_t n) {
+  const int lg = ilog2_exact(n + 1);
+  return lg >= 2 && lg <= 13;
+}
+
+// digit-reversed cell position of every frequency for the DIF plan used on
+// the device (radix-8 stages, then one radix-2 or radix-4 stage)
+std::vector<int> build_perm(int logn) {
+  const int N = 1 << logn;
+  std::vector<int> radices;
+  for (int s = 0; s < logn / 3; ++s) radices.push_back(8);
+  if (logn % 3) radices.push_back(1 << (logn % 3));
+  std::vector<int> perm(N);
+  for (int k = 0; k < N; ++k) {
+    int rem = k, pos = 0, span = N;
+    for (int r : radices) {
+      const int q = rem % r;
+      rem /= r;
+      span /= r;
+      pos += q * span;
+    }
+    perm[k] = pos;
+  }
+  return perm;
+}
+
+int make_tables(int64_t n, Tables& t) {
+  const long double PI = 3.141592653589793238462643383279502884L;
+  if (fft_len_ok(n)) {
+    const int logn = ilog2_exact(n + 1);
+    const int N = 1 << logn;
+    std::vector<double2> tw(N);
+    for (int m = 0; m < N; ++m) {
+      const long double ang = -2.0L * PI * (long double)m / (long double)N;
+      tw[m] = make_double2((double)cosl(ang), (double)sinl(ang));
+    }
+    std::vector<double> sn(N / 2 + 1);
+    for (int j = 0; j <= N / 2; ++j) sn[j] = (double)sinl(PI * (long double)j / (long double)N);
+    std::vector<int> perm = build_perm(logn);
+    FL_CUDA_TRY(cudaMalloc(&t.tw, sizeof(double2) * N));
+    FL_CUDA_TRY(cudaMalloc(&t.sn, sizeof(double) * sn.size()));
+    FL_CUDA_TRY(cudaMalloc(&t.perm, sizeof(int) * N));
+    FL_CUDA_TRY(cudaMemcpy(t.tw, tw.data(), sizeof(double2) * N, cudaMemcpyHostToDevice));
+    FL_CUDA_TRY(cudaMemcpy(t.sn, sn.data(), sizeof(double) * sn.size(), cudaMemcpyHostToDevice));
+    FL_CUDA_TRY(cudaMemcpy(t.perm, perm.data(), sizeof(int) * N, cudaMemcpyHostToDevice));
+  } else {
+    std::vector<double> S((size_t)n * n);
+    const long double N1 = (long double)(n + 1);
+    for (int64_t k = 0; k < n; ++k)
+      for (int64_t j = 0; j < n; ++j) {
+        // reduce (j+1)(k+1) mod 2(n+1) exactly before the sine for accuracy
+        const int64_t m = ((j + 1) * (k + 1)) % (2 * (n + 1));
+        S[(size_t)k * n + j] = (double)sinl(PI * (long double)m / N1);
+      }
+    FL_CUDA_TRY(cudaMalloc(&t.sine, sizeof(double) * S.size()));
+    FL_CUDA_TRY(cudaMemcpy(t.sine, S.data(), sizeof(double) * S.size(), cudaMemcpyHostToDevice));
+  }
+  return FL_OK;
+}
+
+}  // namespace
+
+int get_tables(int64_t n, const Tables** out);
+
+int prepare(int64_t n) {
+  const Tables* t;
+  return get_tables(n, &t);
+}
+
+int get_tables(int64_t n, const Tables** out) {
+  FL_ARG_CHECK(n >= 1, "n must be a positive integer, got %lld", (long long)n);
+  int dev = 0;
+  FL_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto key = std::make_pair(dev, n);
+  auto it = g_tables.find(key);
+  if (it == g_tables.end()) {
+    Tables t;
+    int rc = make_tables(n, t);
+    if (rc != FL_OK) return rc;
+    it = g_tables.emplace(key, t).first;
+  }
+  *out = &it->second;
+  return FL_OK;
+}
+
+namespace {
+
+template <typename K>
+int grid_for(K kernel, int nt, size_t smem, int64_t ntiles, int* grid) {
+  static std::mutex mu;
+  static std::map<const void*, int> occ;
+  int blocks = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = occ.find((const void*)kernel);
+    if (it == occ.end()) {
+      if (smem > 48 * 1024)
+        FL_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      FL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, nt, smem));
+      if (blocks < 1) blocks = 1;
+      occ[(const void*)kernel] = blocks;
+    } else {
+      blocks = it->second;
+    }
+  }
+  const int64_t cap = (int64_t)blocks * sm_count();
+  *grid = (int)(ntiles < cap ? ntiles : cap);
+  if (*grid < 1) *grid = 1;
+  return FL_OK;
+}
+
+template <int LOGN, bool CONTIG, int LOADER, bool MID>
+int launch_fft(DstArgs a, cudaStream_t st) {
+  using S = DstShape<LOGN>;
+  constexpr int C = 2 * S::NFFT;
+  if (CONTIG) {
+    a.ntiles = (a.outer + C - 1) / C;
+    a.nchunks = 1;
+  } else {
+    a.nchunks = (a.inner + C - 1) / C;
+    a.ntiles = a.outer * a.nchunks;
+  }
+  if (a.ntiles == 0) return FL_OK;
+  auto kern = k_dst_fft<LOGN, S::NFFT, S::NT, S::MINB, CONTIG, LOADER, MID>;
+  int grid = 0;
+  int rc = grid_for(kern, S::NT, S::SMEM, a.ntiles, &grid);
+  if (rc) return rc;
+  kern<<<grid, S::NT, S::SMEM, st>>>(a);
+  FL_LAUNCH_CHECK();
+  return FL_OK;
+}
+
+template <bool CONTIG, int LOADER, bool MID>
+int dispatch_fft(int logn, const DstArgs& a, cudaStream_t st) {
+  switch (logn) {
+    case 2: return launch_fft<2, CONTIG, LOADER, MID>(a, st);
+    case 3: return launch_fft<3, CONTIG, LOADER, MID>(a, st);
+    case 4: return launch_fft<4, CONTIG, LOADER, MID>(a, st);
+    case 5: return launch_fft<5, CONTIG, LOADER, MID>(a, st);
+    case 6: return launch_fft<6, CONTIG, LOADER, MID>(a, st);
+    case 7: return launch_fft<7, CONTIG, LOADER, MID>(a, st);
+    case 8: return launch_fft<8, CONTIG, LOADER, MID>(a, st);
+    case 9: return launch_fft<9, CONTIG, LOADER, MID>(a, st);
+    case 10: return launch_fft<10, CONTIG, LOADER, MID>(a, st);
+    case 11: return launch_fft<11, CONTIG, LOADER, MID>(a, st);
+    case 12: return launch_fft<12, CONTIG, LOADER, MID>(a, st);
+    case 13: return launch_fft<13, CONTIG, LOADER, MID>(a, st);
+  }
+  set_error("no FFT plan for log2(N) = %d", logn);
+  return FL_EINVAL;
+}
+
+}  // namespace
+
+// y = scale * F_n x along the middle axis (optionally core-scaled sandwich)
+int dst_mode(const double* x, double* y, int64_t outer, int64_t n, int64_t inner, double scale,
+             const double* core, cudaStream_t st) {
+  FL_ARG_CHECK(outer >= 0 && n >= 1 && inner >= 1, "bad transform shape (%lld, %lld, %lld)",
+               (long long)outer, (long long)n, (long long)inner);
+  if (outer == 0) return FL_OK;
+  const Tables* t = nullptr;
+  int rc = get_tables(n, &t);
+  if (rc) return rc;
+  if (fft_len_ok(n)) {
+    const int logn = ilog2_exact(n + 1);
+    const double nrm = std::sqrt(2.0 / (double)(n + 1));
+    DstArgs a{};
+    a.x = x;
+    a.y = y;
+    a.outer = outer;
+    a.n = n;
+    a.inner = inner;
+    a.core = core;
+    a.tw = t->tw;
+    a.sn = t->sn;
+    a.perm = t->perm;
+    const bool contig = (inner == 1);
+    if (core == nullptr) {
+      a.scale = scale * nrm;
+      return contig ? dispatch_fft<true, LOAD_PLAIN, false>(logn, a, st)
+                    : dispatch_fft<false, LOAD_PLAIN, false>(logn, a, st);
+    }
+    a.scale = scale * nrm * nrm;
+    if (contig) return dispatch_fft<true, LOAD_PLAIN, true>(logn, a, st);
+    // strided fused pass is not instantiated: transform, scale, transform
+    a.scale = nrm;
+    rc = dispatch_fft<false, LOAD_PLAIN, false>(logn, a, st);
+    if (rc) return rc;
+    rc = ew_mul(y, core, y, outer * n * inner, 1.0, st);
+    if (rc) return rc;
+    a.x = y;
+    a.scale = scale * nrm;
+    return dispatch_fft<false, LOAD_PLAIN, false>(logn, a, st);
+  }
+  // dense sine-matrix path: y_o = c * S x_o
+  const double nrm = std::sqrt(2.0 / (double)(n + 1));
+  const double* src = x;
+  double* tmp = nullptr;
+  if (x == y) {
+    FL_CUDA_TRY(cudaMallocAsync(&tmp, sizeof(double) * outer * n * inner, st));
+    FL_CUDA_TRY(cudaMemcpyAsync(tmp, x, sizeof(double) * outer * n * inner, cudaMemcpyDeviceToDevice, st));
+    src = tmp;
+  }
+  if (core == nullptr) {
+    rc = gemm_f64(n, inner, n, scale * nrm, t->sine, n, 1, 0, src, inner, 1, n * inner, 0.0, y, inner, 1,
+                  n * inner, outer, st);
+  } else {
+    rc = gemm_f64(n, inner, n, nrm, t->sine, n, 1, 0, src, inner, 1, n * inner, 0.0, y, inner, 1, n * inner,
+                  outer, st);
+    if (!rc) rc = ew_mul(y, core, y, outer * n * inner, 1.0, st);
+    if (!rc) {
+      if (tmp == nullptr) FL_CUDA_TRY(cudaMallocAsync(&tmp, sizeof(double) * outer * n * inner, st));
+      FL_CUDA_TRY(cudaMemcpyAsync(tmp, y, sizeof(double) * outer * n * inner, cudaMemcpyDeviceToDevice, st));
+      rc = gemm_f64(n, inner, n, scale * nrm, t->sine, n, 1, 0, tmp, inner, 1, n * inner, 0.0, y, inner, 1,
+                    n * inner, outer, st);
+    }
+  }
+  if (tmp) FL_CUDA_TRY(cudaFreeAsync(tmp, st));
+  return rc;
+}
+
+// canonical apply, one mode: out[:, k*S + s] = scale * F(U[:, k] .* Xs[:, s]), out is (n, R*S)
+int dst_kr(const double* U, const double* Xs, double* out, int64_t n, int64_t R, int64_t S, double scale,
+           cudaStream_t st) {
+  FL_ARG_CHECK(n >= 1 && R >= 0 && S >= 0, "bad canonical apply shape");
+  if (R == 0 || S == 0) return FL_OK;
+  const Tables* t = nullptr;
+  int rc = get_tables(n, &t);
+  if (rc) return rc;
+  if (fft_len_ok(n)) {
+    const int logn = ilog2_exact(n + 1);
+    DstArgs a{};
+    a.y = out;
+    a.outer = 1;
+    a.n = n;
+    a.inner = R * S;
+    a.U = U;
+    a.Xs = Xs;
+    a.R = R;
+    a.S = S;
+    a.tw = t->tw;
+    a.sn = t->sn;
+    a.perm = t->perm;
+    a.scale = scale * std::sqrt(2.0 / (double)(n + 1));
+    return dispatch_fft<false, LOAD_KR, false>(logn, a, st);
+  }
+  rc = kr_expand(U, Xs, out, n, R, S, st);
+  if (rc) return rc;
+  return dst_mode(out, out, 1, n, R * S, scale, nullptr, st);
+}
+
+}  // namespace fl

@@ -1,0 +1,37 @@
+// Internal (C++) entry points shared between the translation units.
+#pragma once
+
+#include "common.cuh"
+
+namespace fl {
+
+int prepare(int64_t n);
+
+// y = scale * F x along the middle axis of [outer][n][inner]; with core != nullptr
+// y = scale * F diag(core) F x (core in the layout of x)
+int dst_mode(const double* x, double* y, int64_t outer, int64_t n, int64_t inner, double scale,
+             const double* core, cudaStream_t st);
+
+// out[:, k*S + s] = scale * F(U[:, k] .* Xs[:, s])
+int dst_kr(const double* U, const double* Xs, double* out, int64_t n, int64_t R, int64_t S, double scale,
+           cudaStream_t st);
+
+// C[b] = alpha * A[b] B[b] + beta * C[b] with arbitrary element strides
+int gemm_f64(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t sAm, int64_t sAk,
+             int64_t bA, const double* B, int64_t sBk, int64_t sBn, int64_t bB, double beta, double* C,
+             int64_t sCm, int64_t sCn, int64_t bC, int64_t batch, cudaStream_t st);
+
+int ew_mul(const double* a, const double* b, double* out, int64_t count, double scale, cudaStream_t st);
+
+int kr_expand(const double* U, const double* Xs, double* out, int64_t n, int64_t R, int64_t S, cudaStream_t st);
+
+int core_eval(double* out, int d, const int64_t* dims, const double* const* mu, int tag, double a, double cm,
+              double cp, int recip, cudaStream_t st);
+
+int cp_to_dense(double* out, int d, const int64_t* dims, int64_t R, const double* w, const double* const* U,
+                cudaStream_t st);
+
+int sinc_factor(double* U, const double* mu, int64_t n, const double* t, int64_t R, double rho_min,
+                cudaStream_t st);
+
+}  // namespace fl

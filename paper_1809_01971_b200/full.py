@@ -1,0 +1,132 @@
+"""Full-format (dense n^d) operator functions of the separable Laplacian.
+
+The reference applies F(A) only to canonical tensors; its dense oracle
+(tests/oracles.py:56 dense_apply) is F diag(G) F^T x on a full array.  This
+module is that full-format path on the device: G is a dense core tensor
+resident in HBM (evaluated once per operator by fl_core_eval, or expanded
+from a canonical core by fl_cp_to_dense), and every application is one
+fl_apply_full call: per-mode DST-I passes with the last mode's forward
+transform, core scaling and inverse transform fused into one kernel.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .fracop import CoreFunctionKind, mode_values_device
+from .spectral import EigenSpectrum, transform_axis
+
+__all__ = ["FullOperator", "dense_core", "apply_full", "transform_full", "inner", "norm"]
+
+
+def _shape_check(spectrum, x):
+    if tuple(x.shape) != tuple(spectrum.mode_sizes):
+        raise ValueError("operand dims %r do not match operator dims %r"
+                         % (tuple(x.shape), spectrum.mode_sizes))
+
+
+def dense_core(kind, spectrum, reciprocal=False, device=None):
+    """g(rho) on the full eigenvalue grid (fracop.py:138-148), evaluated on the device."""
+    if not isinstance(kind, CoreFunctionKind):
+        raise ValueError("expected a CoreFunctionKind")
+    _lib.require_cuda()
+    dev = torch.device(device) if device is not None else torch.device("cuda")
+    mus, a = mode_values_device(kind, spectrum, dev)
+    out = torch.empty(spectrum.mode_sizes, dtype=torch.float64, device=dev)
+    _lib.call("fl_core_eval", _lib.ptr(out), spectrum.d, _lib.dims_arr(spectrum.mode_sizes),
+              _lib.ptr_arr(mus), _lib.TAGS.index(kind.tag), float(a), float(kind.coeff_minus),
+              float(kind.coeff_plus), 1 if reciprocal else 0, _lib.stream_ptr())
+    return out
+
+
+def cp_dense(cp, device=None):
+    """Dense expansion of a canonical tensor on the device (tensor.py:217-225)."""
+    dims = cp.dims
+    out = torch.empty(dims, dtype=torch.float64, device=cp.weights.device)
+    _lib.call("fl_cp_to_dense", _lib.ptr(out), len(dims), _lib.dims_arr(dims), cp.rank,
+              _lib.ptr(cp.weights), _lib.ptr_arr(list(cp.factors)), _lib.stream_ptr())
+    return out
+
+
+def _check_operand(x):
+    if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype != torch.float64:
+        raise ValueError("full-format operands are float64 CUDA tensors")
+    if not x.is_contiguous():
+        raise ValueError("full-format operands must be contiguous (C order)")
+
+
+def apply_full(spectrum, core, x, alpha=1.0, out=None):
+    """out = alpha * F diag(core) F x."""
+    _check_operand(x)
+    _shape_check(spectrum, x)
+    y = out if out is not None else torch.empty_like(x)
+    if spectrum.all_sine:
+        _lib.call("fl_apply_full", _lib.ptr(x), _lib.ptr(y), _lib.ptr(core), spectrum.d,
+                  _lib.dims_arr(spectrum.mode_sizes), float(alpha), _lib.stream_ptr())
+        return y
+    z = x
+    for ax, m in enumerate(spectrum.modes):
+        z = transform_axis(m, z.contiguous(), "forward", ax)
+    z = z * core
+    for ax, m in enumerate(spectrum.modes):
+        z = transform_axis(m, z.contiguous(), "inverse", ax)
+    if alpha != 1.0:
+        z = z * alpha
+    y.copy_(z)
+    return y
+
+
+def transform_full(spectrum, x, direction="forward", alpha=1.0, out=None):
+    """Full spectral transform over all modes (forward F or inverse F^T)."""
+    _check_operand(x)
+    _shape_check(spectrum, x)
+    y = out if out is not None else torch.empty_like(x)
+    if spectrum.all_sine:
+        _lib.call("fl_transform_full", _lib.ptr(x), _lib.ptr(y), spectrum.d,
+                  _lib.dims_arr(spectrum.mode_sizes), float(alpha), _lib.stream_ptr())
+        return y
+    z = x
+    for ax, m in enumerate(spectrum.modes):
+        z = transform_axis(m, z.contiguous(), direction, ax)
+    y.copy_(z * alpha if alpha != 1.0 else z)
+    return y
+
+
+class FullOperator:
+    """alpha * F diag(G) F on dense tensors; G resident in HBM."""
+
+    def __init__(self, spectrum, core, alpha=1.0):
+        if not isinstance(spectrum, EigenSpectrum):
+            raise ValueError("expected an EigenSpectrum")
+        if tuple(core.shape) != tuple(spectrum.mode_sizes):
+            raise ValueError("core dims do not match the spectrum")
+        self.spectrum = spectrum
+        self.core = core.contiguous()
+        self.alpha = float(alpha)
+        for m in spectrum.modes:
+            _lib.call("fl_prepare", m.n)
+
+    @classmethod
+    def from_kind(cls, kind, spectrum, reciprocal=False, device=None):
+        return cls(spectrum, dense_core(kind, spectrum, reciprocal, device))
+
+    @classmethod
+    def from_cp(cls, spectrum, cp):
+        return cls(spectrum, cp_dense(cp))
+
+    @property
+    def dims(self):
+        return self.spectrum.mode_sizes
+
+    def __call__(self, x, out=None):
+        return apply_full(self.spectrum, self.core, x, self.alpha, out)
+
+
+def inner(a, b):
+    return float(torch.dot(a.reshape(-1), b.reshape(-1)))
+
+
+def norm(a):
+    return float(torch.linalg.vector_norm(a.reshape(-1)))
