@@ -60,6 +60,13 @@ int fl_prepare(int64_t n);
 int fl_dst1(const double* x, double* y, int64_t outer, int64_t n, int64_t inner,
             double scale, void* stream);
 
+/* Fused operator pass along the middle axis: y = scale * F diag(core) F x
+ * per line (core in the layout of x).  With inner == 1 this is one kernel
+ * (forward DST, core scaling and inverse DST in shared memory); it is the
+ * last-mode pass of fl_apply_full. */
+int fl_dst1_core(const double* x, double* y, const double* core, int64_t outer, int64_t n,
+                 int64_t inner, double scale, void* stream);
+
 /* Dense-eigenbasis transform (spectral.py:316-318 for generalized_mode):
  * y[o] = Q^T x[o] (forward) or Q x[o] (inverse) along the middle axis, Q
  * an (n, n) row-major orthonormal matrix on the device. */

@@ -35,6 +35,7 @@ SIGNATURES = {
     "fl_sm_count": (c_int, []),
     "fl_prepare": (c_int, [c_i64]),
     "fl_dst1": (c_int, [c_vp, c_vp, c_i64, c_i64, c_i64, c_dbl, c_vp]),
+    "fl_dst1_core": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_dbl, c_vp]),
     "fl_basis_apply": (c_int, [c_vp, c_int, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp]),
     "fl_core_eval": (c_int, [c_vp, c_int, P(c_i64), P(c_vp), c_int, c_dbl, c_dbl, c_dbl, c_int, c_vp]),
     "fl_cp_to_dense": (c_int, [c_vp, c_int, P(c_i64), c_i64, c_vp, P(c_vp), c_vp]),

@@ -57,6 +57,12 @@ int fl_dst1(const double* x, double* y, int64_t outer, int64_t n, int64_t inner,
   return dst_mode(x, y, outer, n, inner, scale, nullptr, as_stream(stream));
 }
 
+int fl_dst1_core(const double* x, double* y, const double* core, int64_t outer, int64_t n, int64_t inner,
+                 double scale, void* stream) {
+  FL_ARG_CHECK(core != nullptr, "core tensor required");
+  return dst_mode(x, y, outer, n, inner, scale, core, as_stream(stream));
+}
+
 int fl_basis_apply(const double* Q, int transpose, const double* x, double* y, int64_t outer, int64_t n,
                    int64_t inner, void* stream) {
   FL_ARG_CHECK(n >= 1 && inner >= 1 && outer >= 0, "bad transform shape");

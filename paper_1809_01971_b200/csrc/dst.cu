@@ -154,11 +154,14 @@ int launch_fft(DstArgs a, cudaStream_t st) {
     a.ntiles = a.outer * a.nchunks;
   }
   if (a.ntiles == 0) return FL_OK;
-  auto kern = k_dst_fft<LOGN, S::NFFT, S::NT, S::MINB, CONTIG, LOADER, MID>;
+  constexpr int NT = MID ? S::NT_MID : S::NT;
+  constexpr int MINB = MID ? S::MINB_MID : S::MINB;
+  constexpr size_t SMEM = S::smem(NT);
+  auto kern = k_dst_fft<LOGN, S::NFFT, NT, MINB, CONTIG, LOADER, MID>;
   int grid = 0;
-  int rc = grid_for(kern, S::NT, S::SMEM, a.ntiles, &grid);
+  int rc = grid_for(kern, NT, SMEM, a.ntiles, &grid);
   if (rc) return rc;
-  kern<<<grid, S::NT, S::SMEM, st>>>(a);
+  kern<<<grid, NT, SMEM, st>>>(a);
   FL_LAUNCH_CHECK();
   return FL_OK;
 }
@@ -206,7 +209,6 @@ int dst_mode(const double* x, double* y, int64_t outer, int64_t n, int64_t inner
     a.core = core;
     a.tw = t->tw;
     a.sn = t->sn;
-    a.perm = t->perm;
     const bool contig = (inner == 1);
     if (core == nullptr) {
       a.scale = scale * nrm;
@@ -273,7 +275,6 @@ int dst_kr(const double* U, const double* Xs, double* out, int64_t n, int64_t R,
     a.S = S;
     a.tw = t->tw;
     a.sn = t->sn;
-    a.perm = t->perm;
     a.scale = scale * std::sqrt(2.0 / (double)(n + 1));
     return dispatch_fft<false, LOAD_KR, false>(logn, a, st);
   }

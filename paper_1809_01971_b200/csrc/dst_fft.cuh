@@ -5,18 +5,20 @@
 //   1. load + pre-process (fused): y_j = s_j (x_j + x_{N-j}) + (x_j - x_{N-j})/2,
 //      y_{N-j} = s_j (x_j + x_{N-j}) - (x_j - x_{N-j})/2, s_j = sin(pi j / N),
 //      y_0 = 0, y_{N/2} = 2 x_{N/2}.  Lines 2p and 2p+1 become the real and
-//      imaginary parts of complex sequence p (two real FFTs for the price of one).
-//   2. complex DIF FFT of length N in place, radix-8 stages (+ one radix-2/4),
-//      output in digit-reversed order (perm table maps frequency -> cell).
-//   3. post-process: split the packed spectra, Y^a_k = (C_k + conj C_{N-k})/2,
-//      Y^b_k = (C_k - conj C_{N-k})/(2i); even outputs S_{2k} = -Im Y_k, odd
-//      outputs S_{2k+1} = Re Y_0/2 + sum_{m=1..k} Re Y_m (segmented scan).
-//   4. store (or, for the fused operator pass, scale by the core tensor and run
-//      steps 1-3 a second time before storing).
-// Shared-memory layout: complex cells [pos][p], p (the FFT index within the
-// tile) fastest, XOR-swizzled on p by a fold of pos so that every access
-// pattern (row stores, strided butterflies, digit-reversed reads) stays close
-// to conflict-free.
+//      imaginary parts of complex sequence p (two real FFTs for one complex FFT).
+//   2. complex DIF FFT of length N in place, radix-8 stages (+ one radix-2/4);
+//      frequency k ends up in cell perm(k) (digit reversal, computed inline).
+//   3. post-process in place: Y^a_k = (C_k + conj C_{N-k})/2,
+//      Y^b_k = (C_k - conj C_{N-k})/(2i); the even output S_{2k} = -Im Y_k goes
+//      to cell perm(k), Re Y_k to cell perm(N-k); a segmented scan over k then
+//      turns Re Y into the odd outputs S_{2k+1} = Re Y_0/2 + sum_{m<=k} Re Y_m.
+//   4. store row j from its cell (even rows from perm(j/2), odd rows from
+//      perm(N - (j-1)/2)); the fused operator pass instead scales by the core
+//      tensor and runs steps 1-3 again before storing.
+// Shared-memory layout: complex cells [pos][p], p (FFT index in the tile)
+// fastest.  Contiguous-line tiles (which are transposed on load) XOR-swizzle
+// p by a fold of pos; the fold is XOR-linear so butterfly addresses need one
+// XOR-immediate per access.
 #pragma once
 
 #include "common.cuh"
@@ -39,7 +41,6 @@ struct DstArgs {
   // per-N tables
   const double2* tw;  // N twiddles exp(-2 pi i m / N)
   const double* sn;   // N/2 + 1 values sin(pi j / N)
-  const int* perm;    // N: frequency -> cell position
 };
 
 template <int LOGN>
@@ -49,26 +50,38 @@ struct FftPlan {
   static constexpr int rlog(int s) { return s < LOGN / 3 ? 3 : LOGN % 3; }
 };
 
-template <int LOGF>
-__device__ __forceinline__ int swz_key(int pos) {
-  if constexpr (LOGF == 0) {
-    return 0;
-  } else {
-    int k = 0;
+// cell holding frequency k after the DIF stages (digit reversal of k)
+template <int LOGN>
+__device__ __forceinline__ int perm_of(int k) {
+  using P = FftPlan<LOGN>;
+  int pos = 0, lg = LOGN;
 #pragma unroll
-    for (int sh = 0; sh < 14; sh += LOGF) k ^= (pos >> sh);
-    return k & ((1 << LOGF) - 1);
+  for (int s = 0; s < P::NST; ++s) {
+    const int rl = P::rlog(s);
+    lg -= rl;
+    pos |= (k & ((1 << rl) - 1)) << lg;
+    k >>= rl;
   }
+  return pos;
 }
 
-template <int NFFT>
+template <int LOGN, int LOGF, bool SWZ>
+__host__ __device__ constexpr int swz_key(int pos) {
+  if (!SWZ || LOGF == 0) return 0;
+  int k = 0;
+  for (int sh = 0; sh < LOGN; sh += LOGF) k ^= (pos >> sh);
+  return k & ((1 << LOGF) - 1);
+}
+
+template <int LOGN, int NFFT, bool SWZ>
 struct Cells {
   static constexpr int LOGF = NFFT == 1 ? 0 : NFFT == 2 ? 1 : NFFT == 4 ? 2 : NFFT == 8 ? 3 : 4;
   double2* D;
-  __device__ __forceinline__ int idx(int pos, int p) const { return pos * NFFT + (p ^ swz_key<LOGF>(pos)); }
+  __device__ __forceinline__ static int idx(int pos, int p) {
+    return pos * NFFT + (p ^ swz_key<LOGN, LOGF, SWZ>(pos));
+  }
   __device__ __forceinline__ double2 ld(int pos, int p) const { return D[idx(pos, p)]; }
   __device__ __forceinline__ void st(int pos, int p, double2 v) const { D[idx(pos, p)] = v; }
-  // real element (line l, row j)
   __device__ __forceinline__ double& re(int l, int j) const {
     return reinterpret_cast<double*>(D)[2 * idx(j, l >> 1) + (l & 1)];
   }
@@ -92,12 +105,12 @@ __device__ __forceinline__ void dft4(double2& a0, double2& a1, double2& a2, doub
 
 __device__ __forceinline__ void dft8(double2 (&a)[8]) {
   constexpr double r = 0.70710678118654752440084436210485;
-  dft4(a[0], a[2], a[4], a[6]);  // E0..E3 in a0,a2,a4,a6
-  dft4(a[1], a[3], a[5], a[7]);  // O0..O3 in a1,a3,a5,a7
+  dft4(a[0], a[2], a[4], a[6]);
+  dft4(a[1], a[3], a[5], a[7]);
   double2 o1 = a[3], o2 = a[5], o3 = a[7];
-  o1 = make_double2((o1.x + o1.y) * r, (o1.y - o1.x) * r);  // * (1 - i)/sqrt2
-  o2 = cmul_mi(o2);                                         // * -i
-  o3 = make_double2((o3.y - o3.x) * r, -(o3.x + o3.y) * r); // * (-1 - i)/sqrt2
+  o1 = make_double2((o1.x + o1.y) * r, (o1.y - o1.x) * r);   // * (1 - i)/sqrt2
+  o2 = cmul_mi(o2);                                          // * -i
+  o3 = make_double2((o3.y - o3.x) * r, -(o3.x + o3.y) * r);  // * (-1 - i)/sqrt2
   double2 e0 = a[0], e1 = a[2], e2 = a[4], e3 = a[6], o0 = a[1];
   a[0] = cadd(e0, o0);
   a[4] = csub(e0, o0);
@@ -116,14 +129,17 @@ __device__ __forceinline__ void dftR(double2 (&a)[1 << RL]) {
   if constexpr (RL == 3) dft8(a);
 }
 
-// one DIF stage: sub-length L = 2^LGL, radix R = 2^RL, stride st = L / R
-template <int LOGN, int NFFT, int NT, int LGL, int RL>
-__device__ __forceinline__ void fft_stage(const Cells<NFFT>& cs, const double2* __restrict__ tw) {
+// one DIF stage: sub-length L = 2^LGL, radix R = 2^RL, stride st = L / R.
+// Point t of butterfly (block, j) sits at base | (t << LGST): the bits of
+// base and t*ST are disjoint, so the swizzle key splits into key(base) ^ K(t).
+template <int LOGN, int NFFT, int NT, bool SWZ, int LGL, int RL>
+__device__ __forceinline__ void fft_stage(const Cells<LOGN, NFFT, SWZ>& cs, const double2* __restrict__ tw) {
+  using CS = Cells<LOGN, NFFT, SWZ>;
   constexpr int N = 1 << LOGN;
   constexpr int R = 1 << RL;
   constexpr int LGST = LGL - RL;
   constexpr int ST = 1 << LGST;
-  constexpr int NB = NFFT * (N / R);  // butterflies in this stage
+  constexpr int NB = NFFT * (N / R);
   constexpr int PER = (NB + NT - 1) / NT;
 #pragma unroll
   for (int it = 0; it < PER; ++it) {
@@ -133,261 +149,571 @@ __device__ __forceinline__ void fft_stage(const Cells<NFFT>& cs, const double2* 
       const int bi = b / NFFT;
       const int j = bi & (ST - 1);
       const int base = ((bi >> LGST) << LGL) + j;
+      const int pk = p ^ swz_key<LOGN, CS::LOGF, SWZ>(base);
+      double2* row = cs.D + base * NFFT;
       double2 v[R];
 #pragma unroll
-      for (int t = 0; t < R; ++t) v[t] = cs.ld(base + t * ST, p);
+      for (int t = 0; t < R; ++t) v[t] = row[t * ST * NFFT + (pk ^ swz_key<LOGN, CS::LOGF, SWZ>(t << LGST))];
       dftR<RL>(v);
       if constexpr (LGST > 0) {
 #pragma unroll
-        for (int q = 1; q < R; ++q) {
-          const double2 w = __ldg(&tw[(j * q) << (LOGN - LGL)]);
-          v[q] = cmul(v[q], w);
-        }
+        for (int q = 1; q < R; ++q) v[q] = cmul(v[q], __ldg(&tw[(j * q) << (LOGN - LGL)]));
       }
 #pragma unroll
-      for (int q = 0; q < R; ++q) cs.st(base + q * ST, p, v[q]);
+      for (int q = 0; q < R; ++q) row[q * ST * NFFT + (pk ^ swz_key<LOGN, CS::LOGF, SWZ>(q << LGST))] = v[q];
     }
   }
   __syncthreads();
 }
 
-template <int LOGN, int NFFT, int NT, int S, int LGL>
-__device__ __forceinline__ void fft_rec(const Cells<NFFT>& cs, const double2* __restrict__ tw) {
+template <int LOGN, int NFFT, int NT, bool SWZ, int S, int LGL>
+__device__ __forceinline__ void fft_rec(const Cells<LOGN, NFFT, SWZ>& cs, const double2* __restrict__ tw) {
   if constexpr (S < FftPlan<LOGN>::NST) {
     constexpr int RL = FftPlan<LOGN>::rlog(S);
-    fft_stage<LOGN, NFFT, NT, LGL, RL>(cs, tw);
-    fft_rec<LOGN, NFFT, NT, S + 1, LGL - RL>(cs, tw);
+    fft_stage<LOGN, NFFT, NT, SWZ, LGL, RL>(cs, tw);
+    fft_rec<LOGN, NFFT, NT, SWZ, S + 1, LGL - RL>(cs, tw);
   }
 }
 
-// exclusive scan of v over aligned groups of G consecutive threads
-template <int G, int NT>
-__device__ __forceinline__ double2 group_excl_scan(double2 v, double* scr) {
-  constexpr int W = G < 32 ? G : 32;
-  const int lane = threadIdx.x & 31;
-  double2 x = v;
+// frequency held by cell c after the DIF stages (inverse digit reversal)
+template <int LOGN>
+__device__ __forceinline__ int perm_inv(int c) {
+  using P = FftPlan<LOGN>;
+  int k = 0, lg = LOGN, sh = 0;
 #pragma unroll
-  for (int d = 1; d < W; d <<= 1) {
-    const double yx = __shfl_up_sync(0xffffffffu, x.x, d, W);
-    const double yy = __shfl_up_sync(0xffffffffu, x.y, d, W);
-    if ((lane & (W - 1)) >= d) {
-      x.x += yx;
-      x.y += yy;
+  for (int s = 0; s < P::NST; ++s) {
+    const int rl = P::rlog(s);
+    lg -= rl;
+    k |= ((c >> lg) & ((1 << rl) - 1)) << sh;
+    sh += rl;
+  }
+  return k;
+}
+
+// DIT stage = transpose of the DIF stage with the same (LGL, RL): twiddles
+// before the butterfly.  Running the DIF stages transposed in reverse order
+// maps digit-reversed input (cell perm(j) holds x_j) to natural-order output.
+template <int LOGN, int NFFT, int NT, bool SWZ, int LGL, int RL>
+__device__ __forceinline__ void dit_stage(const Cells<LOGN, NFFT, SWZ>& cs, const double2* __restrict__ tw) {
+  using CS = Cells<LOGN, NFFT, SWZ>;
+  constexpr int N = 1 << LOGN;
+  constexpr int R = 1 << RL;
+  constexpr int LGST = LGL - RL;
+  constexpr int ST = 1 << LGST;
+  constexpr int NB = NFFT * (N / R);
+  constexpr int PER = (NB + NT - 1) / NT;
+#pragma unroll
+  for (int it = 0; it < PER; ++it) {
+    const int b = threadIdx.x + it * NT;
+    if (NB % NT == 0 || b < NB) {
+      const int p = b % NFFT;
+      const int bi = b / NFFT;
+      const int j = bi & (ST - 1);
+      const int base = ((bi >> LGST) << LGL) + j;
+      const int pk = p ^ swz_key<LOGN, CS::LOGF, SWZ>(base);
+      double2* row = cs.D + base * NFFT;
+      double2 v[R];
+#pragma unroll
+      for (int t = 0; t < R; ++t) v[t] = row[t * ST * NFFT + (pk ^ swz_key<LOGN, CS::LOGF, SWZ>(t << LGST))];
+      if constexpr (LGST > 0) {
+#pragma unroll
+        for (int q = 1; q < R; ++q) v[q] = cmul(v[q], __ldg(&tw[(j * q) << (LOGN - LGL)]));
+      }
+      dftR<RL>(v);
+#pragma unroll
+      for (int q = 0; q < R; ++q) row[q * ST * NFFT + (pk ^ swz_key<LOGN, CS::LOGF, SWZ>(q << LGST))] = v[q];
     }
   }
-  if constexpr (G <= 32) {
+  __syncthreads();
+}
+
+// DIF stage index S -> log2 of its sub-length
+template <int LOGN, int S>
+struct StageLGL {
+  static constexpr int value = S == 0 ? LOGN : StageLGL<LOGN, (S > 0 ? S - 1 : 0)>::value - FftPlan<LOGN>::rlog(S - 1);
+};
+template <int LOGN>
+struct StageLGL<LOGN, 0> {
+  static constexpr int value = LOGN;
+};
+
+// DIT stages for DIF stages S, S-1, ..., 0
+template <int LOGN, int NFFT, int NT, bool SWZ, int S>
+__device__ __forceinline__ void dit_rec(const Cells<LOGN, NFFT, SWZ>& cs, const double2* __restrict__ tw) {
+  if constexpr (S >= 0) {
+    dit_stage<LOGN, NFFT, NT, SWZ, StageLGL<LOGN, S>::value, FftPlan<LOGN>::rlog(S)>(cs, tw);
+    dit_rec<LOGN, NFFT, NT, SWZ, S - 1>(cs, tw);
+  }
+}
+
+// post-process geometry: thread t -> FFT p = t % NFFT, rank g = t / NFFT,
+// rank g owns frequencies [g*KPT, (g+1)*KPT)
+template <int LOGN, int NFFT, int NT>
+struct PostShape {
+  static constexpr int H = (1 << LOGN) / 2;
+  static constexpr int G0 = NT / NFFT;
+  static constexpr int G = G0 < H ? G0 : H;
+  static constexpr int KPT = H / G;
+  static constexpr int NW = NT / 32;
+};
+
+// exclusive scan over ranks g (threads with equal p, stride NFFT)
+template <int LOGN, int NFFT, int NT>
+__device__ __forceinline__ double2 rank_excl_scan(double2 v, double2* scr) {
+  using PS = PostShape<LOGN, NFFT, NT>;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  double2 x = v;
+  if constexpr (NFFT < 32) {
+#pragma unroll
+    for (int d = NFFT; d < 32; d <<= 1) {
+      const double yx = __shfl_up_sync(0xffffffffu, x.x, d);
+      const double yy = __shfl_up_sync(0xffffffffu, x.y, d);
+      if (lane >= d) {
+        x.x += yx;
+        x.y += yy;
+      }
+    }
+  }
+  if constexpr (PS::NW == 1) {
     return make_double2(x.x - v.x, x.y - v.y);
   } else {
-    const int warp = threadIdx.x >> 5;
-    if (lane == 31) {
-      scr[2 * warp] = x.x;
-      scr[2 * warp + 1] = x.y;
-    }
+    // warp totals per p live in the last NFFT lanes
+    if (lane >= 32 - NFFT) scr[warp * NFFT + (lane & (NFFT - 1))] = x;
     __syncthreads();
-    constexpr int WPG = G / 32;
-    const int first = (warp / WPG) * WPG;
+    const int p = threadIdx.x & (NFFT - 1);
     double ox = 0.0, oy = 0.0;
-    for (int w = first; w < warp; ++w) {
-      ox += scr[2 * w];
-      oy += scr[2 * w + 1];
+    for (int w = 0; w < warp; ++w) {
+      const double2 s = scr[w * NFFT + p];
+      ox += s.x;
+      oy += s.y;
     }
     __syncthreads();
     return make_double2(x.x - v.x + ox, x.y - v.y + oy);
   }
 }
 
-// post-process the packed spectra into natural-order DST outputs (times sc)
-template <int LOGN, int NFFT, int NT>
-__device__ __forceinline__ void dst_post(const Cells<NFFT>& cs, const int* __restrict__ perm,
-                                         double sc, double* scr) {
+// compile-time digit reversal (host/device constexpr twin of perm_of)
+template <int LOGN>
+__host__ __device__ constexpr int perm_c(int k) {
+  int pos = 0, lg = LOGN;
+  for (int s = 0; s < FftPlan<LOGN>::NST; ++s) {
+    const int rl = FftPlan<LOGN>::rlog(s);
+    lg -= rl;
+    pos |= (k & ((1 << rl) - 1)) << lg;
+    k >>= rl;
+  }
+  return pos;
+}
+
+// Cells of frequency k and N-k for k = k0 + m*S (S a power of two, k0 < S):
+// digit reversal acts on disjoint bit fields, so perm(k) = perm(k0) | perm(m*S)
+// and, with N - k = ~(k - 1), perm(N - k) = (N-1) - (perm(k0-1) | perm(m*S)).
+struct KCells {
+  int pe;   // perm(k0)
+  int po;   // (N-1) - perm(k0-1), unused when k0 == 0
+  bool z;   // k0 == 0
+};
+
+template <int LOGN>
+__device__ __forceinline__ KCells kcells(int k0) {
+  KCells c;
+  c.pe = perm_of<LOGN>(k0);
+  c.z = (k0 == 0);
+  c.po = (1 << LOGN) - 1 - perm_of<LOGN>(k0 - 1);
+  return c;
+}
+
+// ms is a compile-time constant after loop unrolling; perm_c folds away
+template <int LOGN>
+__device__ __forceinline__ int cell_even(const KCells& c, int ms) {
+  return c.pe | perm_c<LOGN>(ms);
+}
+
+template <int LOGN>
+__device__ __forceinline__ int cell_odd(const KCells& c, int ms) {
   constexpr int N = 1 << LOGN;
-  constexpr int H = N / 2;
-  constexpr int G0 = NT / NFFT;
-  constexpr int G = G0 < H ? G0 : H;
-  constexpr int KPT = H / G;
-  const int t = threadIdx.x;
-  const bool active = t < NFFT * G;
-  const int p = t / G;
-  const int g = t % G;
-  double ea[KPT], eb[KPT], oa[KPT], ob[KPT];
+  return c.z ? perm_c<LOGN>((N - ms) & (N - 1)) : c.po - perm_c<LOGN>(ms);
+}
+
+// in-place post-process (see header); leaves even outputs in perm(k) and odd
+// outputs in perm(N-k), unscaled.  Rank g owns k in [g*KPT, (g+1)*KPT), i.e.
+// k = i + g*KPT with the roles of (k0, m*S) swapped: perm(k) = perm(i) | A.
+template <int LOGN, int NFFT, int NT, bool SWZ, bool NAT = false>
+__device__ __forceinline__ void dst_post(const Cells<LOGN, NFFT, SWZ>& cs, double2* scr) {
+  using PS = PostShape<LOGN, NFFT, NT>;
+  using CS = Cells<LOGN, NFFT, SWZ>;
+  constexpr int N = 1 << LOGN;
+  constexpr int K = PS::KPT;
+  const int p = threadIdx.x % NFFT;
+  const int g = threadIdx.x / NFFT;
+  const bool active = g < PS::G;
+  // NAT: spectrum in natural order (cell k holds frequency k)
+  const int A = NAT ? g * K : perm_of<LOGN>(g * K);
+  const int B = (g == 0) ? 0 : (NAT ? N - g * K : (N - 1 - perm_of<LOGN>(g * K - 1)));
   double2 tot = make_double2(0.0, 0.0);
+  // P1: split the packed spectra pairwise (k, N-k); R_k summed on the fly
   if (active) {
 #pragma unroll
-    for (int i = 0; i < KPT; ++i) {
-      const int k = g * KPT + i;
-      const double2 ck = cs.ld(__ldg(&perm[k]), p);
-      const double2 cm = cs.ld(__ldg(&perm[(N - k) & (N - 1)]), p);
-      ea[i] = 0.5 * (cm.y - ck.y);
-      eb[i] = 0.5 * (ck.x - cm.x);
-      double ra = 0.5 * (ck.x + cm.x);
-      double rb = 0.5 * (ck.y + cm.y);
-      if (k == 0) {
-        ra *= 0.5;
-        rb *= 0.5;
+    for (int i = 0; i < K; ++i) {
+      const int ck_pos = NAT ? A + i : (A | perm_c<LOGN>(i));
+      const int cm_pos = (i == 0) ? B : (NAT ? N - A - i : (N - 1 - (A | perm_c<LOGN>(i - 1))));
+      const int ik = CS::idx(ck_pos, p), im = CS::idx(cm_pos, p);
+      const double2 ck = cs.D[ik];
+      const double2 cm = cs.D[im];
+      const double2 e = make_double2(0.5 * (cm.y - ck.y), 0.5 * (ck.x - cm.x));
+      double2 r = make_double2(0.5 * (ck.x + cm.x), 0.5 * (ck.y + cm.y));
+      if (i == 0 && g == 0) {
+        r.x *= 0.5;
+        r.y *= 0.5;
+        cs.D[ik] = r;  // cell 0 seeds S_1; S_0 = 0 is implicit
+      } else {
+        cs.D[ik] = e;
+        cs.D[im] = r;
       }
-      tot.x += ra;
-      tot.y += rb;
-      oa[i] = tot.x;
-      ob[i] = tot.y;
+      tot.x += r.x;
+      tot.y += r.y;
     }
   }
-  const double2 off = group_excl_scan<G, NT>(active ? tot : make_double2(0.0, 0.0), scr);
-  __syncthreads();
+  // P2: segmented prefix sum of Re Y over k -> odd outputs
+  double2 run = rank_excl_scan<LOGN, NFFT, NT>(tot, scr);
   if (active) {
 #pragma unroll
-    for (int i = 0; i < KPT; ++i) {
-      const int k = g * KPT + i;
-      cs.st(2 * k, p, make_double2(ea[i] * sc, eb[i] * sc));
-      cs.st(2 * k + 1, p, make_double2((oa[i] + off.x) * sc, (ob[i] + off.y) * sc));
+    for (int i = 0; i < K; ++i) {
+      const int cm_pos = (i == 0) ? B : (NAT ? N - A - i : (N - 1 - (A | perm_c<LOGN>(i - 1))));
+      const int im = CS::idx(cm_pos, p);
+      const double2 r = cs.D[im];
+      run.x += r.x;
+      run.y += r.y;
+      cs.D[im] = run;
     }
   }
   __syncthreads();
 }
+
+// cell position of natural output row j after dst_post (j in [1, N-1])
+template <int LOGN>
+__device__ __forceinline__ int out_pos(int j) {
+  constexpr int N = 1 << LOGN;
+  return (j & 1) ? perm_of<LOGN>((N - (j >> 1)) & (N - 1)) : perm_of<LOGN>(j >> 1);
+}
+
+template <int LOGN, int NFFT, bool SWZ>
+__device__ __forceinline__ double out_elem(const Cells<LOGN, NFFT, SWZ>& cs, int l, int j) {
+  return reinterpret_cast<const double*>(cs.D)[2 * Cells<LOGN, NFFT, SWZ>::idx(out_pos<LOGN>(j), l >> 1) + (l & 1)];
+}
+
+// per-tile addressing: element (l, j) (j in [1, n]) at base + l*LS + (j-1)*JS
+struct TileAddr {
+  int64_t base;  // element offset of (0, 1)
+  int64_t JS;
+  int LS;
+  int lmax;  // lines [0, lmax) are valid
+  int64_t c0;
+};
 
 template <bool CONTIG, int C>
-__device__ __forceinline__ bool line_ok(const DstArgs& a, int64_t tile, int l, int64_t& off0, int64_t& jstride) {
+__device__ __forceinline__ TileAddr tile_addr(const DstArgs& a, int64_t tile) {
+  TileAddr t;
   if (CONTIG) {
-    const int64_t L = tile * C + l;
-    off0 = L * a.n;
-    jstride = 1;
-    return L < a.outer;
+    const int64_t L0 = tile * C;
+    t.base = L0 * a.n;
+    t.JS = 1;
+    t.LS = (int)a.n;
+    const int64_t rem = a.outer - L0;
+    t.lmax = (int)(rem < C ? rem : C);
+    t.c0 = 0;
   } else {
     const int64_t o = tile / a.nchunks;
-    const int64_t c = (tile % a.nchunks) * C + l;
-    off0 = o * a.n * a.inner + c;
-    jstride = a.inner;
-    return c < a.inner;
+    const int64_t c0 = (tile - o * a.nchunks) * C;
+    t.base = o * a.n * a.inner + c0;
+    t.JS = a.inner;
+    t.LS = 1;
+    const int64_t rem = a.inner - c0;
+    t.lmax = (int)(rem < C ? rem : C);
+    t.c0 = c0;
   }
+  return t;
 }
+
+// Work split shared by the load, fused-core and store phases: items (l, k),
+// k in [0, H) (a row pair), C*H items over NT threads, PER per thread.
+// Strided tiles: l = t % C fixed, k = t / C + it * (NT / C).
+// Contiguous tiles: k = t % H (+ multiples of NT when NT < H), l varies.
+template <int LOGN, int NFFT, int NT, bool CONTIG>
+struct Split {
+  static constexpr int N = 1 << LOGN;
+  static constexpr int H = N / 2;
+  static constexpr int C = 2 * NFFT;
+  static constexpr int ITEMS = C * H;
+  static constexpr int PER = (ITEMS + NT - 1) / NT;
+  // k = k0 + MS(it), l = l0 + LD(it)
+  __device__ __forceinline__ static void base(int t, int& k0, int& l0) {
+    if (CONTIG) {
+      k0 = (NT >= H) ? (t % H) : t;
+      l0 = (NT >= H) ? (t / H) : 0;
+    } else {
+      k0 = t / C;
+      l0 = t % C;
+    }
+  }
+  __host__ __device__ static constexpr int MS(int it) {
+    return CONTIG ? ((NT >= H) ? 0 : (it % (H / NT)) * NT) : it * (NT / C);
+  }
+  __host__ __device__ static constexpr int LD(int it) {
+    return CONTIG ? ((NT >= H) ? it * (NT / H) : it / (H / NT)) : 0;
+  }
+  __host__ __device__ static constexpr int KS() {  // S of the k = k0 + m*S form
+    return CONTIG ? ((NT >= H) ? H : NT) : (NT / C);
+  }
+  __device__ __forceinline__ static bool ok(int t, int it) { return ITEMS % NT == 0 || t + it * NT < ITEMS; }
+};
 
 template <int LOADER>
-__device__ __forceinline__ double load_elem(const DstArgs& a, int64_t off0, int64_t row, int64_t jstride) {
+__device__ __forceinline__ double load_elem(const DstArgs& a, const TileAddr& ta, int l, int row) {
   if constexpr (LOADER == LOAD_PLAIN) {
-    return __ldg(&a.x[off0 + row * jstride]);
+    return __ldg(&a.x[ta.base + (int64_t)l * ta.LS + (int64_t)row * ta.JS]);
   } else {
-    // off0 == c (column of the virtual R*S matrix, outer == 1), jstride == R*S
-    const int64_t c = off0;
+    const int64_t c = ta.c0 + l;
     const int64_t k = c / a.S, s = c - k * a.S;
-    return __ldg(&a.U[row * a.R + k]) * __ldg(&a.Xs[row * a.S + s]);
+    return __ldg(&a.U[(int64_t)row * a.R + k]) * __ldg(&a.Xs[(int64_t)row * a.S + s]);
   }
 }
 
-// stage 1: global -> smem with the DST-I pre-processing fused in.
-// MODE 0: load from x; MODE 1: smem already holds a transform, scale by core.
-template <bool CONTIG, int C, int H>
-__device__ __forceinline__ void item_lj(int item, int& l, int& jj) {
-  if (CONTIG) {
-    l = item / H;
-    jj = item % H;
+// element (l, row j) of the natural-order layout
+template <int LOGN, int NFFT, bool SWZ>
+__device__ __forceinline__ double& nat(const Cells<LOGN, NFFT, SWZ>& cs, int l, int j) {
+  return cs.re(l, j);
+}
+
+// DST-I pre-processing of rows (j, N-j) from values (va, vb)
+template <int LOGN, int NFFT, bool SWZ>
+__device__ __forceinline__ void pre_pair(const Cells<LOGN, NFFT, SWZ>& cs, const double* __restrict__ sn, int l, int j,
+                                         double va, double vb) {
+  constexpr int H = (1 << LOGN) / 2;
+  if (j == H) {
+    cs.re(l, H) = 2.0 * va;
   } else {
-    l = item % C;
-    jj = item / C;
+    const double s = __ldg(&sn[j]);
+    const double sum = s * (va + vb), dif = 0.5 * (va - vb);
+    cs.re(l, j) = sum + dif;
+    cs.re(l, (1 << LOGN) - j) = sum - dif;
   }
 }
 
-template <int LOGN, int NFFT, int NT, bool CONTIG, int LOADER, int MODE>
-__device__ __forceinline__ void dst_pre(const DstArgs& a, const Cells<NFFT>& cs, int64_t tile) {
+// stage 1: global -> smem with the DST-I pre-processing fused in.  Item
+// (l, k) covers rows j = k + 1 and N - j.  All of a thread's loads are issued
+// before any is consumed; addresses advance by per-item constant strides.
+template <int LOGN, int NFFT, int NT, bool CONTIG, int LOADER>
+__device__ __forceinline__ void dst_load_pre(const DstArgs& a, const Cells<LOGN, NFFT, CONTIG>& cs,
+                                             const TileAddr& ta) {
+  using SP = Split<LOGN, NFFT, NT, CONTIG>;
+  constexpr int N = SP::N, H = SP::H, PER = SP::PER;
+  constexpr int B = PER < 8 ? PER : 8;
+  static_assert(PER % B == 0, "batch must divide the per-thread item count");
+  int k0, l0;
+  SP::base(threadIdx.x, k0, l0);
+  if constexpr (LOADER == LOAD_PLAIN) {
+    const double* xp = a.x + ta.base + (int64_t)l0 * ta.LS;
+    const double* pa = xp + (int64_t)k0 * ta.JS;           // row j - 1 = k
+    const double* pb = xp + (int64_t)(N - 2 - k0) * ta.JS; // row N - j - 1
+#pragma unroll
+    for (int it0 = 0; it0 < PER; it0 += B) {
+      double xa[B], xb[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int it = it0 + u;
+        const int l = l0 + SP::LD(it);
+        const int k = k0 + SP::MS(it);
+        const int64_t off = (int64_t)SP::LD(it) * ta.LS + (int64_t)SP::MS(it) * ta.JS;
+        xa[u] = 0.0;
+        xb[u] = 0.0;
+        if (SP::ok(threadIdx.x, it) && l < ta.lmax) {
+          xa[u] = __ldg(pa + off);
+          if (k + 1 < H) xb[u] = __ldg(pb + (int64_t)SP::LD(it) * ta.LS - (int64_t)SP::MS(it) * ta.JS);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int it = it0 + u;
+        if (SP::ok(threadIdx.x, it)) pre_pair(cs, a.sn, l0 + SP::LD(it), k0 + SP::MS(it) + 1, xa[u], xb[u]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int it0 = 0; it0 < PER; it0 += B) {
+      double xa[B], xb[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int it = it0 + u;
+        const int l = l0 + SP::LD(it);
+        const int j = k0 + SP::MS(it) + 1;
+        xa[u] = 0.0;
+        xb[u] = 0.0;
+        if (SP::ok(threadIdx.x, it) && l < ta.lmax) {
+          xa[u] = load_elem<LOADER>(a, ta, l, j - 1);
+          if (j < H) xb[u] = load_elem<LOADER>(a, ta, l, N - j - 1);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int it = it0 + u;
+        if (SP::ok(threadIdx.x, it)) pre_pair(cs, a.sn, l0 + SP::LD(it), k0 + SP::MS(it) + 1, xa[u], xb[u]);
+      }
+    }
+  }
+  for (int l = threadIdx.x; l < SP::C; l += NT) cs.re(l, 0) = 0.0;
+}
+
+// value of natural row j (1 <= j <= N-1) of line l after dst_post
+template <int LOGN, int NFFT, bool SWZ>
+__device__ __forceinline__ double post_val(const Cells<LOGN, NFFT, SWZ>& cs, int l, int cell) {
+  return reinterpret_cast<const double*>(cs.D)[2 * Cells<LOGN, NFFT, SWZ>::idx(cell, l >> 1) + (l & 1)];
+}
+
+// fused operator pass, step 1: scale the post-processed forward transform by
+// the core in place (cells perm(k) / perm(N-k) hold rows 2k / 2k+1), with the
+// coalesced store mapping for the core loads.
+template <int LOGN, int NFFT, int NT, bool CONTIG>
+__device__ __forceinline__ void dst_core_scale(const DstArgs& a, const Cells<LOGN, NFFT, CONTIG>& cs,
+                                               const TileAddr& ta) {
+  using SP = Split<LOGN, NFFT, NT, CONTIG>;
+  using CS = Cells<LOGN, NFFT, CONTIG>;
+  constexpr int PER = SP::PER;
+  int k0, l0;
+  SP::base(threadIdx.x, k0, l0);
+  const KCells kc = kcells<LOGN>(k0);
+  const double* cb = a.core + ta.base + (int64_t)l0 * ta.LS;
+  double ce_v[PER], co_v[PER];
+#pragma unroll
+  for (int it = 0; it < PER; ++it) {
+    const int l = l0 + SP::LD(it);
+    const int k = k0 + SP::MS(it);
+    ce_v[it] = 0.0;
+    co_v[it] = 0.0;
+    if (SP::ok(threadIdx.x, it) && l < ta.lmax) {
+      const double* cl = cb + (int64_t)SP::LD(it) * ta.LS;
+      co_v[it] = __ldg(cl + (int64_t)(2 * k) * ta.JS);
+      if (k > 0) ce_v[it] = __ldg(cl + (int64_t)(2 * k - 1) * ta.JS);
+    }
+  }
+  double* D = reinterpret_cast<double*>(cs.D);
+#pragma unroll
+  for (int it = 0; it < PER; ++it) {
+    const int l = l0 + SP::LD(it);
+    if (SP::ok(threadIdx.x, it)) {
+      const int io = 2 * CS::idx(cell_odd<LOGN>(kc, SP::MS(it)), l >> 1) + (l & 1);
+      D[io] *= co_v[it];
+      if (k0 + SP::MS(it) > 0) {
+        const int ie = 2 * CS::idx(cell_even<LOGN>(kc, SP::MS(it)), l >> 1) + (l & 1);
+        D[ie] *= ce_v[it];
+      }
+    }
+  }
+}
+
+// fused operator pass, step 2: first DIT stage (transpose of the last DIF
+// stage: sub-length R, unit stride, no twiddles) whose inputs are gathered
+// from the core-scaled spectrum with the DST-I pre-processing applied on the
+// fly.  Cell c of the DIT input holds y_j, j = perm_inv(c); y_j needs rows
+// j and N - j, which sit in cells out_pos(j) and out_pos(N - j).  All reads
+// finish before the barrier; each thread then writes its own butterfly.
+template <int LOGN, int NFFT, int NT, bool CONTIG>
+__device__ __forceinline__ void dit_gather_stage(const DstArgs& a, const Cells<LOGN, NFFT, CONTIG>& cs) {
+  using CS = Cells<LOGN, NFFT, CONTIG>;
   constexpr int N = 1 << LOGN;
   constexpr int H = N / 2;
-  constexpr int C = 2 * NFFT;
-  constexpr int ITEMS = C * H;
-  constexpr int PER = (ITEMS + NT - 1) / NT;
-  constexpr int B = PER < 4 ? PER : 4;  // items whose loads are batched
-  static_assert(PER % B == 0, "batch must divide the per-thread item count");
-  for (int it0 = 0; it0 < PER; it0 += B) {
-    double xa[B], xb[B];
-    bool ok[B];
+  constexpr int RL = FftPlan<LOGN>::rlog(FftPlan<LOGN>::NST - 1);
+  constexpr int R = 1 << RL;
+  constexpr int NB = NFFT * (N / R);
+  constexpr int PER = (NB + NT - 1) / NT;
+  double2 v[PER][R];
 #pragma unroll
-    for (int u = 0; u < B; ++u) {
-      const int item = threadIdx.x + (it0 + u) * NT;
-      int l, jj;
-      item_lj<CONTIG, C, H>(item, l, jj);
-      const int j = jj + 1;
-      int64_t off0, js;
-      ok[u] = (ITEMS % NT == 0 || item < ITEMS) && line_ok<CONTIG, C>(a, tile, l, off0, js);
-      xa[u] = 0.0;
-      xb[u] = 0.0;
-      if (MODE == 0) {
-        if (ok[u]) {
-          xa[u] = load_elem<LOADER>(a, off0, j - 1, js);
-          if (j < H) xb[u] = load_elem<LOADER>(a, off0, N - j - 1, js);
-        }
-      } else if (ok[u]) {
-        xa[u] = __ldg(&a.core[off0 + (int64_t)(j - 1) * js]);
-        if (j < H) xb[u] = __ldg(&a.core[off0 + (int64_t)(N - j - 1) * js]);
-      }
-    }
+  for (int it = 0; it < PER; ++it) {
+    const int b = threadIdx.x + it * NT;
+    if (NB % NT == 0 || b < NB) {
+      const int p = b % NFFT;
+      const int base = (b / NFFT) * R;
 #pragma unroll
-    for (int u = 0; u < B; ++u) {
-      const int item = threadIdx.x + (it0 + u) * NT;
-      if (ITEMS % NT == 0 || item < ITEMS) {
-        int l, jj;
-        item_lj<CONTIG, C, H>(item, l, jj);
-        const int j = jj + 1;
-        double va = xa[u], vb = xb[u];
-        if (MODE == 1) {
-          // xa/xb hold core values; scale the forward transform held in smem
-          va = ok[u] ? cs.re(l, j) * va : 0.0;
-          vb = (ok[u] && j < H) ? cs.re(l, N - j) * vb : 0.0;
+      for (int t = 0; t < R; ++t) {
+        const int j = perm_inv<LOGN>(base + t);
+        // y_j = s_j (x_j + x_{N-j}) + (x_j - x_{N-j})/2 holds for every j in [1, N)
+        double2 y = make_double2(0.0, 0.0);
+        if (j != 0) {
+          const double2 xa = cs.ld(out_pos<LOGN>(j), p);
+          const double2 xb = (j == H) ? xa : cs.ld(out_pos<LOGN>(N - j), p);
+          const double s = __ldg(&a.sn[j < H ? j : N - j]);
+          y = make_double2(fma(s, xa.x + xb.x, 0.5 * (xa.x - xb.x)), fma(s, xa.y + xb.y, 0.5 * (xa.y - xb.y)));
         }
-        if (j == H) {
-          cs.re(l, H) = 2.0 * va;
-        } else {
-          const double s = __ldg(&a.sn[j]);
-          const double sum = s * (va + vb), dif = 0.5 * (va - vb);
-          cs.re(l, j) = sum + dif;
-          cs.re(l, N - j) = sum - dif;
-        }
+        v[it][t] = y;
       }
+      dftR<RL>(v[it]);
     }
   }
-  if (MODE == 0) {
-    for (int l = threadIdx.x; l < C; l += NT) cs.re(l, 0) = 0.0;
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < PER; ++it) {
+    const int b = threadIdx.x + it * NT;
+    if (NB % NT == 0 || b < NB) {
+      const int p = b % NFFT;
+      const int base = (b / NFFT) * R;
+#pragma unroll
+      for (int q = 0; q < R; ++q) cs.st(base + q, p, v[it][q]);
+    }
   }
+  __syncthreads();
 }
 
-template <int LOGN, int NFFT, int NT, bool CONTIG>
-__device__ __forceinline__ void dst_store(const DstArgs& a, const Cells<NFFT>& cs, int64_t tile) {
-  constexpr int N = 1 << LOGN;
-  constexpr int C = 2 * NFFT;
-  constexpr int ROWS = N - 1;
-  constexpr int ITEMS = C * ROWS;
-  constexpr int PER = (ITEMS + NT - 1) / NT;
-#pragma unroll 4
+// store: item (l, k) writes rows 2k (k >= 1) and 2k+1 from cells perm(k) and
+// perm(N-k), addresses linear in the unrolled item index.
+template <int LOGN, int NFFT, int NT, bool CONTIG, bool NAT = false>
+__device__ __forceinline__ void dst_store(const DstArgs& a, const Cells<LOGN, NFFT, CONTIG>& cs,
+                                          const TileAddr& ta) {
+  using SP = Split<LOGN, NFFT, NT, CONTIG>;
+  constexpr int PER = SP::PER;
+  const double sc = a.scale;
+  int k0, l0;
+  SP::base(threadIdx.x, k0, l0);
+  const KCells kc = kcells<LOGN>(k0);
+  double* yb = a.y + ta.base + (int64_t)l0 * ta.LS;
+#pragma unroll
   for (int it = 0; it < PER; ++it) {
-    const int item = threadIdx.x + it * NT;
-    if (item < ITEMS) {
-      int l, j;
-      if (CONTIG) {
-        l = item / ROWS;
-        j = item % ROWS + 1;
-      } else {
-        l = item % C;
-        j = item / C + 1;
-      }
-      int64_t off0, js;
-      if (line_ok<CONTIG, C>(a, tile, l, off0, js)) a.y[off0 + (int64_t)(j - 1) * js] = cs.re(l, j);
+    const int l = l0 + SP::LD(it);
+    const int k = k0 + SP::MS(it);
+    if (SP::ok(threadIdx.x, it) && l < ta.lmax) {
+      double* yl = yb + (int64_t)SP::LD(it) * ta.LS;
+      const int ce = NAT ? k : cell_even<LOGN>(kc, SP::MS(it));
+      const int co = NAT ? ((SP::N - k) & (SP::N - 1)) : cell_odd<LOGN>(kc, SP::MS(it));
+      // row 2k+1 -> offset 2k, row 2k -> offset 2k-1
+      yl[(int64_t)(2 * k) * ta.JS] = sc * post_val(cs, l, co);
+      if (k > 0) yl[(int64_t)(2 * k - 1) * ta.JS] = sc * post_val(cs, l, ce);
     }
   }
 }
 
 template <int LOGN, int NFFT, int NT, int MINB, bool CONTIG, int LOADER, bool MIDCORE>
 __global__ void __launch_bounds__(NT, MINB) k_dst_fft(const DstArgs a) {
+  using CS = Cells<LOGN, NFFT, CONTIG>;
+  constexpr int C = 2 * NFFT;
   extern __shared__ __align__(16) double smem_dst[];
-  Cells<NFFT> cs{reinterpret_cast<double2*>(smem_dst)};
-  double* scr = smem_dst + 2 * (1 << LOGN) * NFFT;
+  CS cs{reinterpret_cast<double2*>(smem_dst)};
+  double2* scr = reinterpret_cast<double2*>(smem_dst + 2 * (1 << LOGN) * NFFT);
   for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
-    dst_pre<LOGN, NFFT, NT, CONTIG, LOADER, 0>(a, cs, tile);
+    const TileAddr ta = tile_addr<CONTIG, C>(a, tile);
+    dst_load_pre<LOGN, NFFT, NT, CONTIG, LOADER>(a, cs, ta);
     __syncthreads();
-    fft_rec<LOGN, NFFT, NT, 0, LOGN>(cs, a.tw);
+    fft_rec<LOGN, NFFT, NT, CONTIG, 0, LOGN>(cs, a.tw);
+    dst_post<LOGN, NFFT, NT, CONTIG>(cs, scr);
     if constexpr (MIDCORE) {
-      dst_post<LOGN, NFFT, NT>(cs, a.perm, 1.0, scr);
-      dst_pre<LOGN, NFFT, NT, CONTIG, LOADER, 1>(a, cs, tile);
+      dst_core_scale<LOGN, NFFT, NT, CONTIG>(a, cs, ta);
       __syncthreads();
-      fft_rec<LOGN, NFFT, NT, 0, LOGN>(cs, a.tw);
+      dit_gather_stage<LOGN, NFFT, NT, CONTIG>(a, cs);
+      dit_rec<LOGN, NFFT, NT, CONTIG, FftPlan<LOGN>::NST - 2>(cs, a.tw);
+      dst_post<LOGN, NFFT, NT, CONTIG, true>(cs, scr);
+      dst_store<LOGN, NFFT, NT, CONTIG, true>(a, cs, ta);
+    } else {
+      dst_store<LOGN, NFFT, NT, CONTIG>(a, cs, ta);
     }
-    dst_post<LOGN, NFFT, NT>(cs, a.perm, a.scale, scr);
-    dst_store<LOGN, NFFT, NT, CONTIG>(a, cs, tile);
     __syncthreads();
   }
 }
@@ -399,7 +725,11 @@ struct DstShape {
   static constexpr int NFFT = LOGN <= 8 ? 16 : (LOGN >= 12 ? 1 : (8 >> (LOGN - 9)));
   static constexpr int NT = LOGN >= 13 ? 1024 : (LOGN >= 8 ? 512 : (LOGN <= 5 ? 128 : 256));
   static constexpr int MINB = LOGN >= 13 ? 1 : (LOGN >= 8 ? 2 : (LOGN <= 5 ? 8 : 4));
-  static constexpr size_t SMEM = size_t(16) * (size_t(1) << LOGN) * NFFT + size_t(16) * (NT / 32);
+  // the fused operator pass stages its whole tile in registers across a
+  // barrier: twice the threads halves the per-thread share
+  static constexpr int NT_MID = NT;
+  static constexpr int MINB_MID = MINB;
+  static constexpr size_t smem(int nt) { return size_t(16) * (size_t(1) << LOGN) * NFFT + size_t(16) * NFFT * (nt / 32); }
 };
 
 }  // namespace fl
