@@ -107,6 +107,29 @@ int fl_apply_full(const double* x, double* y, const double* core, int d,
 int fl_transform_full(const double* x, double* y, int d, const int64_t* dims,
                       double alpha, void* stream);
 
+/* ---- canonical format --------------------------------------------------
+ * One mode of the canonical operator application, fracop.apply
+ * (fracop.py:474-495): out (n, R*S) with column k*S + s equal to
+ * scale * F(U[:, k] .* Xs[:, s]); U is the (n, R) core factor, Xs the
+ * already transformed (n, S) operand factor.  The Hadamard expansion is
+ * formed while loading the DST tile (no n x R*S intermediate). */
+int fl_cp_apply_mode(const double* U, const double* Xs, double* out, int64_t n,
+                     int64_t R, int64_t S, double scale, void* stream);
+
+/* Hadamard product of per-mode Gram matrices, the kernel of cp_inner
+ * (tensor.py:156-167): H[i][j] = prod_l sum_r A_l[r][i] B_l[r][j] for d
+ * factor pairs A_l (n_l, Ra), B_l (n_l, Rb); H is (Ra, Rb) row-major. */
+int fl_cp_gram(int d, const int64_t* n, const double* const* A, int64_t Ra,
+               const double* const* B, int64_t Rb, double* H, void* stream);
+
+/* Column norms of an (n, R) matrix (cp_normalize, tensor.py:180-197). */
+int fl_col_norms(const double* U, int64_t n, int64_t R, double* out, void* stream);
+
+/* V = U with columns divided by nrm; zero columns become e_1
+ * (tensor.py:189-195). */
+int fl_col_scale(const double* U, const double* nrm, int64_t n, int64_t R,
+                 double* V, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -229,3 +229,12 @@ def pcg_dense(matvec, precond, b, tol, k_max):
         p = z + (rz_new / rz) * p
         rz = rz_new
     return x, hist, it, False
+
+
+def reciprocal_svd_core(tag, mus, a, cm, cp, r):
+    """Rank-r reciprocal core by dense SVD (the 2D preconditioner route,
+    fracop.py:392-402 with reciprocal=True and a fixed-rank spec) as a dense array."""
+    G = dense_core(tag, mus, a, cm, cp, reciprocal=True)
+    U, s, Vt = np.linalg.svd(G, full_matrices=False)
+    k = min(int(r), int(np.count_nonzero(s > 0.0)))
+    return (U[:, :k] * s[:k]) @ Vt[:k]

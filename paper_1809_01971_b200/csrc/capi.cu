@@ -131,4 +131,26 @@ int fl_transform_full(const double* x, double* y, int d, const int64_t* dims, do
   return dst_mode(y, y, 1, n0, n1 * n2, alpha, nullptr, st);
 }
 
+int fl_cp_apply_mode(const double* U, const double* Xs, double* out, int64_t n, int64_t R, int64_t S, double scale,
+                     void* stream) {
+  return dst_kr(U, Xs, out, n, R, S, scale, as_stream(stream));
+}
+
+int fl_cp_gram(int d, const int64_t* n, const double* const* A, int64_t Ra, const double* const* B, int64_t Rb,
+               double* H, void* stream) {
+  FL_ARG_CHECK(d >= 1 && d <= 3, "order must be 1..3");
+  FL_ARG_CHECK(Ra >= 0 && Rb >= 0, "ranks must be nonnegative");
+  return gram_hadamard(d, n, A, Ra, B, Rb, H, as_stream(stream));
+}
+
+int fl_col_norms(const double* U, int64_t n, int64_t R, double* out, void* stream) {
+  FL_ARG_CHECK(n >= 1 && R >= 0, "bad matrix shape");
+  return col_norms(U, n, R, out, as_stream(stream));
+}
+
+int fl_col_scale(const double* U, const double* nrm, int64_t n, int64_t R, double* V, void* stream) {
+  FL_ARG_CHECK(n >= 1 && R >= 0, "bad matrix shape");
+  return col_scale(U, nrm, n, R, V, as_stream(stream));
+}
+
 }  // extern "C"

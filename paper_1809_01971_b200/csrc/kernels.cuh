@@ -31,6 +31,13 @@ int core_eval(double* out, int d, const int64_t* dims, const double* const* mu, 
 int cp_to_dense(double* out, int d, const int64_t* dims, int64_t R, const double* w, const double* const* U,
                 cudaStream_t st);
 
+int gram_hadamard(int d, const int64_t* n, const double* const* A, int64_t Ra, const double* const* B, int64_t Rb,
+                  double* H, cudaStream_t st);
+
+int col_norms(const double* U, int64_t n, int64_t R, double* out, cudaStream_t st);
+
+int col_scale(const double* U, const double* nrm, int64_t n, int64_t R, double* V, cudaStream_t st);
+
 int sinc_factor(double* U, const double* mu, int64_t n, const double* t, int64_t R, double rho_min,
                 cudaStream_t st);
 

@@ -1,0 +1,150 @@
+"""Canonical-format path on the GPU vs golden vectors from the reference."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1809_01971_b200 as fl
+from paper_1809_01971_b200 import fracop as flop
+
+pytestmark = pytest.mark.gpu
+G = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def load(name):
+    return np.load(os.path.join(G, name + ".npz"))
+
+
+def rel(a, b):
+    a = a.cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def cp(data, prefix, d):
+    return fl.CpTensor(data[prefix + "_w"], [data["%s_f%d" % (prefix, l)] for l in range(d)])
+
+
+def test_dst_apply_golden():
+    g = load("spectral")
+    for n in (1, 2, 3, 5, 7, 9, 12, 15, 16, 31, 63, 127, 255, 511):
+        got = fl.dst_apply(fl.laplacian_mode(n), g["x_%d" % n])
+        assert rel(got, g["dst_%d" % n]) <= 1e-13
+
+
+def test_dense_cores_golden():
+    g = load("cores")
+    for d, n in ((2, 9), (3, 7)):
+        spec = fl.laplacian_spectrum(n, d)
+        for tag in ("g1", "g2", "g3", "g4"):
+            for agg in ("sum-then-power", "power-then-sum"):
+                kind = fl.CoreFunctionKind(tag, 0.5, aggregation=agg, coeff_minus=1.3, coeff_plus=0.7)
+                for rec in (False, True):
+                    got = flop.dense_core_dev(kind, spec, rec)
+                    assert rel(got, g["core_d%d_n%d_%s_%s_%d" % (d, n, tag, agg, int(rec))]) <= 1e-14
+
+
+def test_sinc_golden():
+    g = load("cores")
+    spec = fl.laplacian_spectrum(32, 2)
+    for M in (4, 9, 16):
+        op = fl.sinc_inverse_power(spec, 0.5, M)
+        assert op.rank == 2 * M + 1
+        assert rel(op.core.weights, g["sinc_M%d_w" % M]) <= 1e-14
+        for l in range(2):
+            assert rel(op.core.factors[l], g["sinc_M%d_f%d" % (M, l)]) <= 1e-14
+        assert op.achieved_error == pytest.approx(float(g["sinc_M%d_err" % M]), rel=1e-8)
+
+
+@pytest.mark.parametrize("case", [(2, 16, "g2"), (2, 15, "g1"), (3, 9, "g2"), (3, 15, "g4")])
+def test_apply_golden(case):
+    d, n, tag = case
+    g = load("apply")
+    key = "ap_d%d_n%d_%s" % case
+    spec = fl.laplacian_spectrum(n, d)
+    alpha = 1.0 if tag == "g1" else 0.5
+    diag = fl.DiagOpFunction(spec, fl.CoreFunctionKind(tag, alpha), cp(g, key + "_core", d), 0.0)
+    y = fl.LowRankOperator(diag)(cp(g, key + "_x", d))
+    assert y.rank == int(g[key + "_rank"])
+    assert rel(fl.cp_to_dense(y), g[key + "_y"]) <= 1e-12
+
+
+def test_inner_norm_normalize():
+    rng = np.random.default_rng(5)
+    for dims in ((7, 6), (4, 3, 5), (40, 33, 17)):
+        wa, fa = rng.standard_normal(3), [rng.standard_normal((n, 3)) for n in dims]
+        wb, fb = rng.standard_normal(70), [rng.standard_normal((n, 70)) for n in dims]
+        a, b = fl.CpTensor(wa, fa), fl.CpTensor(wb, fb)
+        want = oracle.cp_inner(wa, fa, wb, fb)
+        assert fl.cp_inner(a, b) == pytest.approx(want, rel=1e-12)
+        an = fl.cp_normalize(b)
+        assert rel(fl.cp_to_dense(an), oracle.cp_to_dense(wb, fb)) <= 1e-13
+        assert fl.cp_norm(a) == pytest.approx(np.linalg.norm(oracle.cp_to_dense(wa, fa)), rel=1e-12)
+    z = fl.CpTensor(np.array([1.0, 3.0]), [np.array([[0.0, 1.0], [0.0, 2.0]]), np.array([[1.0, 1.0], [1.0, 0.0]])])
+    zn = fl.cp_normalize(z)
+    assert float(zn.weights[0]) == 0.0
+
+
+def test_trunc_golden():
+    g = load("trunc")
+    for i in range(4):
+        key = "tr%d" % i
+        x = cp(g, key + "_x", g[key + "_dense"].ndim)
+        tol = float(g[key + "_tol"])
+        out = fl.trunc(x, fl.TruncationSpec(tolerance=tol))
+        dense = g[key + "_dense"]
+        assert out.rank == int(g[key + "_rank"])
+        assert rel(fl.cp_to_dense(out), dense) <= 1.01 * tol + 1e-13
+        assert rel(fl.cp_to_dense(out), g[key + "_out"]) <= 2.0 * tol + 1e-13
+
+
+def test_solve_control_2d_golden():
+    g = load("solve")
+    n, d = 12, 2
+    spec = fl.laplacian_spectrum(n, d)
+    y_d = fl.DesignFunction("two-bumps").evaluate((n,) * d)
+    cfg = fl.SolverConfig(alpha=0.5, beta=1.0, gamma=1e-2, eps=1e-10, precond_rank=8, residual_tol=1e-10, k_max=60)
+    u, rep = fl.solve_control(y_d, cfg, spec)
+    assert rep.converged
+    assert abs(rep.iterations - int(g["c2_iters"])) <= 1
+    assert rel(fl.cp_to_dense(u), g["c2_u"]) <= 1e-8
+
+
+def test_solve_state_3d_golden():
+    g = load("solve")
+    n, d = 9, 3
+    spec = fl.laplacian_spectrum(n, d)
+    y_d = fl.DesignFunction("gaussian-bump").evaluate((n,) * d)
+    cfg = fl.SolverConfig(alpha=0.5, beta=2.0, gamma=1e-3, eps=1e-10, precond_rank=8, residual_tol=1e-9, k_max=60)
+    y = fl.solve_state(y_d, cfg, spec)
+    assert rel(fl.cp_to_dense(y), g["s3_y"]) <= 1e-8
+
+
+def test_config0_canonical_golden():
+    """BASELINE configs[0] through the canonical API (the reference's own path)."""
+    g = load("config0")
+    n, d = 255, 2
+    spec = fl.laplacian_spectrum(n, d)
+    y = cp(g, "y", d)
+    cfg = fl.SolverConfig(alpha=0.5, beta=1e-3, eps=1e-10, precond_rank=6, residual_tol=1e-8, k_max=100)
+    u, rep = fl.solve_control(y, cfg, spec)
+    assert rep.converged
+    assert abs(rep.iterations - int(g["iters"])) <= 1
+    want = oracle.cp_to_dense(g["u_w"], [g["u_f0"], g["u_f1"]])
+    assert rel(fl.cp_to_dense(u), want) <= 1e-8
+
+
+@pytest.mark.parametrize("n3", [15, 31])
+def test_solve_control_3d_golden(n3):
+    g = load("solve")
+    key = "c3_n%d" % n3
+    spec = fl.laplacian_spectrum(n3, 3)
+    y = cp(g, key + "_y", 3)
+    cfg = fl.SolverConfig(alpha=float(g[key + "_alpha"]), beta=1e-2, eps=1e-8, precond_rank=6,
+                          residual_tol=1e-6, k_max=60)
+    u, rep = fl.solve_control(y, cfg, spec)
+    assert rep.converged
+    assert abs(rep.iterations - int(g[key + "_iters"])) <= 1
+    assert rel(fl.cp_to_dense(u), g[key + "_u"]) <= 1e-6
