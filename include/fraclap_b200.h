@@ -130,6 +130,30 @@ int fl_col_norms(const double* U, int64_t n, int64_t R, double* out, void* strea
 int fl_col_scale(const double* U, const double* nrm, int64_t n, int64_t R,
                  double* V, void* stream);
 
+/* ---- full-format PCG (solver.py:116-180 on dense tensors) --------------
+ * Spectral-space PCG for the operator F diag(A) F with preconditioner
+ * F diag(P) F: b_hat = F b is the transformed right-hand side, x_hat the
+ * transformed solution (x = F x_hat); r and p are N-double work arrays.
+ * The whole solve is ONE cooperative persistent launch: no host round trip
+ * per iteration.  hist (device, k_max + 1 doubles) receives the relative
+ * residual history ||r_k|| / ||b||; status (device, 4 ints) receives
+ * [iterations, converged, breakdown iteration, breakdown kind (1: <R,Z> <= 0,
+ * 2: <P,S> <= 0)], the reference's PcgBreakdownError conditions. */
+int fl_pcg_spectral(const double* b_hat, double* x_hat, double* r, double* p,
+                    const double* A, const double* P, int64_t N, double tol,
+                    int k_max, double* hist, int* status, void* stream);
+
+#define FL_PCG_WORK 8192
+/* One streaming phase of the same iteration for the slab-partitioned
+ * multi-GPU solve (the caller all-reduces `out` across ranks):
+ *   phase 0: x = 0, r = b, p = P b;         out = [b.b, b.Pb, p.Ap]
+ *   phase 1: x += s p, r -= s A p;          out = [r.r, r.Pr]
+ *   phase 2: p = P r + s p;                 out = [p.Ap]
+ * work: FL_PCG_WORK doubles zeroed once before the first call. */
+int fl_pcg_phase(int phase, const double* b_hat, double* x_hat, double* r, double* p,
+                 const double* A, const double* P, int64_t N, double s, double* out,
+                 double* work, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -153,4 +153,15 @@ int fl_col_scale(const double* U, const double* nrm, int64_t n, int64_t R, doubl
   return col_scale(U, nrm, n, R, V, as_stream(stream));
 }
 
+int fl_pcg_spectral(const double* b_hat, double* x_hat, double* r, double* p, const double* A, const double* P,
+                    int64_t N, double tol, int k_max, double* hist, int* status, void* stream) {
+  return pcg_spectral(b_hat, x_hat, r, p, A, P, N, tol, k_max, hist, status, as_stream(stream));
+}
+
+int fl_pcg_phase(int phase, const double* b_hat, double* x_hat, double* r, double* p, const double* A,
+                 const double* P, int64_t N, double s, double* out, double* work, void* stream) {
+  FL_ARG_CHECK(N >= 0, "bad PCG size");
+  return pcg_phase(phase, b_hat, x_hat, r, p, A, P, N, s, out, work, as_stream(stream));
+}
+
 }  // extern "C"

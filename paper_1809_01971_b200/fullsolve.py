@@ -1,0 +1,145 @@
+"""Full-format control and state solves (dense n^d tensors on the device).
+
+The reference solves the control equation (solver.py:203-231)
+    (beta A^-alpha + (gamma/beta) A^alpha) u = y_design
+by PCG with the rank-r Kronecker preconditioner (solver.py:183-189) in
+canonical arithmetic.  On dense tensors both the system operator and the
+preconditioner are F diag(.) F with the same orthonormal DST-I basis F, so
+the PCG iteration runs on spectral coefficients (fl_pcg_spectral: one
+cooperative persistent kernel for the whole solve).  mode="nodal" runs the
+same iteration with an explicit F diag F application per operator call (the
+literal Algorithm 1 on dense tensors) for validation.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .fracop import CoreFunctionKind, dense_core_dev
+from .full import apply_full, cp_dense, dense_core, transform_full
+from .solver import PcgBreakdownError, PcgReport, SolverConfig, build_preconditioner
+
+__all__ = ["control_cores", "pcg_full", "solve_control_full", "solve_state_full"]
+
+
+def _control_kind(cfg):
+    return CoreFunctionKind("g2", cfg.alpha, coeff_minus=float(cfg.beta), coeff_plus=float(cfg.gamma) / float(cfg.beta))
+
+
+def control_cores(cfg, spectrum, precond="kronecker", seed=0):
+    """Dense system core A = g2(beta, gamma/beta) and preconditioner core P.
+
+    precond: "kronecker" (the reference's rank-r reciprocal core, expanded to
+    dense), "exact" (1/g2, i.e. g3), or "identity".
+    """
+    kind = _control_kind(cfg)
+    A = dense_core(kind, spectrum)
+    if precond == "kronecker":
+        pre = build_preconditioner(kind, spectrum, cfg.precond_rank, seed=seed)
+        P = cp_dense(pre.diag.core)
+    elif precond == "exact":
+        P = dense_core(kind, spectrum, reciprocal=True)
+    elif precond == "identity":
+        P = torch.ones_like(A)
+    else:
+        raise ValueError("precond must be 'kronecker', 'exact' or 'identity'")
+    return A, P
+
+
+def pcg_full(spectrum, A, P, b, tol, k_max, mode="spectral"):
+    """PCG for F diag(A) F x = b with preconditioner F diag(P) F on dense tensors.
+
+    Returns (x, PcgReport).  Raises PcgBreakdownError on <R,Z> <= 0 or
+    <P,S> <= 0 exactly as the reference (solver.py:154-159).
+    """
+    if mode == "nodal":
+        return _pcg_nodal(spectrum, A, P, b, tol, k_max)
+    if mode != "spectral":
+        raise ValueError("mode must be 'spectral' or 'nodal'")
+    dev = b.device
+    N = b.numel()
+    bh = transform_full(spectrum, b)
+    xh = torch.empty_like(bh)
+    r = torch.empty_like(bh)
+    p = torch.empty_like(bh)
+    hist = torch.zeros(int(k_max) + 1, dtype=torch.float64, device=dev)
+    status = torch.zeros(4, dtype=torch.int32, device=dev)
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record()
+    _lib.call("fl_pcg_spectral", _lib.ptr(bh), _lib.ptr(xh), _lib.ptr(r), _lib.ptr(p), _lib.ptr(A), _lib.ptr(P),
+              N, float(tol), int(k_max), _lib.ptr(hist), _lib.ptr(status), _lib.stream_ptr())
+    end.record()
+    x = transform_full(spectrum, xh)
+    st = status.cpu().numpy()
+    its, conv, bk_it, bk_kind = (int(v) for v in st)
+    if bk_kind:
+        raise PcgBreakdownError(bk_it, float("nan"), what="<R, Z>" if bk_kind == 1 else "<P, S>")
+    torch.cuda.synchronize()
+    secs = start.elapsed_time(end) / 1e3
+    residuals = hist[: its + 1].cpu().numpy().tolist() if its else [float(hist[0])]
+    per = secs / its if its else 0.0
+    return x, PcgReport(iterations=its, residuals=residuals, final_rank=0, converged=bool(conv),
+                        iteration_seconds=[per] * its, seconds_per_iteration=per)
+
+
+def _pcg_nodal(spectrum, A, P, b, tol, k_max):
+    """The literal iteration with F diag F applications (validation path)."""
+    def fun(v):
+        return apply_full(spectrum, A, v.contiguous())
+
+    def pre(v):
+        return apply_full(spectrum, P, v.contiguous())
+
+    def dot(u, v):
+        return float(torch.dot(u.reshape(-1), v.reshape(-1)))
+
+    norm_b = dot(b, b) ** 0.5
+    x = torch.zeros_like(b)
+    if norm_b == 0.0:
+        return x, PcgReport(iterations=0, residuals=[0.0], converged=True)
+    r = b.clone()
+    residuals = [1.0]
+    z = pre(r)
+    p = z.clone()
+    rz = dot(r, z)
+    its, conv = 0, False
+    for k in range(1, int(k_max) + 1):
+        if rz <= 0.0:
+            raise PcgBreakdownError(k, rz, what="<R, Z>")
+        s = fun(p)
+        ps = dot(p, s)
+        if ps <= 0.0:
+            raise PcgBreakdownError(k, ps)
+        step = rz / ps
+        x.add_(p, alpha=step)
+        r.add_(s, alpha=-step)
+        rel = dot(r, r) ** 0.5 / norm_b
+        residuals.append(rel)
+        its = k
+        if rel <= tol:
+            conv = True
+            break
+        z = pre(r)
+        rzn = dot(r, z)
+        p = z + (rzn / rz) * p
+        rz = rzn
+    return x, PcgReport(iterations=its, residuals=residuals, converged=conv)
+
+
+def solve_control_full(y_design, cfg, spectrum, precond="kronecker", mode="spectral", seed=0, cores=None):
+    """Optimal control on dense tensors: PCG on the g2 system (solver.py:203-216)."""
+    if not isinstance(cfg, SolverConfig):
+        raise ValueError("expected a SolverConfig")
+    if tuple(y_design.shape) != tuple(spectrum.mode_sizes):
+        raise ValueError("design function dims do not match the spectrum")
+    A, P = cores if cores is not None else control_cores(cfg, spectrum, precond, seed)
+    return pcg_full(spectrum, A, P, y_design, cfg.residual_tol, cfg.k_max, mode)
+
+
+def solve_state_full(y_design, cfg, spectrum):
+    """y = (I + (gamma/beta^2) A^(2 alpha))^-1 y_design: one g4 application (solver.py:245-249)."""
+    kind = CoreFunctionKind("g4", cfg.alpha, coeff_plus=float(cfg.gamma) / float(cfg.beta) ** 2)
+    return apply_full(spectrum, dense_core(kind, spectrum), y_design)

@@ -1,0 +1,95 @@
+"""Full-format PCG (spectral persistent kernel and nodal) vs the reference and the oracle."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1809_01971_b200 as fl
+from paper_1809_01971_b200 import fullsolve, full
+
+pytestmark = pytest.mark.gpu
+G = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def rel(a, b):
+    a = a.cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
+    b = b.cpu().numpy() if isinstance(b, torch.Tensor) else np.asarray(b)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.mark.parametrize("mode", ["spectral", "nodal"])
+def test_config0_full_format_matches_reference(mode):
+    """BASELINE configs[0] on dense tensors vs the reference's canonical solve."""
+    g = np.load(os.path.join(G, "config0.npz"))
+    n = 255
+    spec = fl.laplacian_spectrum(n, 2)
+    y = torch.tensor(oracle.cp_to_dense(g["y_w"], [g["y_f0"], g["y_f1"]]), device="cuda")
+    cfg = fl.SolverConfig(alpha=0.5, beta=1e-3, eps=1e-10, precond_rank=6, residual_tol=1e-8, k_max=100)
+    u, rep = fullsolve.solve_control_full(y, cfg, spec, mode=mode)
+    assert rep.converged
+    assert abs(rep.iterations - int(g["iters"])) <= 1
+    want = oracle.cp_to_dense(g["u_w"], [g["u_f0"], g["u_f1"]])
+    assert rel(u, want) <= 1e-8
+    assert rep.residuals[-1] <= 1e-8
+
+
+def test_spectral_equals_nodal_3d():
+    n = 31
+    spec = fl.laplacian_spectrum(n, 3)
+    w, f = oracle.gaussian_bumps(n, 3, 8, seed=3)
+    y = torch.tensor(oracle.cp_to_dense(w, f), device="cuda")
+    cfg = fl.SolverConfig(alpha=0.75, beta=1e-2, precond_rank=5, residual_tol=1e-10, k_max=60)
+    cores = fullsolve.control_cores(cfg, spec)
+    u1, r1 = fullsolve.solve_control_full(y, cfg, spec, mode="spectral", cores=cores)
+    u2, r2 = fullsolve.solve_control_full(y, cfg, spec, mode="nodal", cores=cores)
+    assert r1.iterations == r2.iterations
+    assert rel(u1, u2) <= 1e-10
+    for a, b in zip(r1.residuals, r2.residuals):
+        assert a == pytest.approx(b, rel=1e-6, abs=1e-14)
+    # the CPU oracle with the same cores
+    A, P = (c.cpu().numpy() for c in cores)
+    x, hist, it, ok = oracle.pcg_dense(lambda v: oracle.apply_full(A, v), lambda v: oracle.apply_full(P, v),
+                                       y.cpu().numpy(), 1e-10, 60)
+    assert ok and it == r1.iterations
+    assert rel(u1, x) <= 1e-10
+
+
+def test_exact_preconditioner_converges_in_one_iteration():
+    n = 63
+    spec = fl.laplacian_spectrum(n, 3)
+    y = torch.randn((n, n, n), dtype=torch.float64, device="cuda")
+    cfg = fl.SolverConfig(alpha=0.5, beta=1e-2, residual_tol=1e-10, k_max=10)
+    u, rep = fullsolve.solve_control_full(y, cfg, spec, precond="exact")
+    assert rep.converged and rep.iterations == 1
+
+
+def test_breakdown_names_the_iteration():
+    n = 15
+    spec = fl.laplacian_spectrum(n, 2)
+    A = -torch.ones((n, n), dtype=torch.float64, device="cuda")
+    P = torch.ones_like(A)
+    b = torch.randn((n, n), dtype=torch.float64, device="cuda")
+    with pytest.raises(fl.PcgBreakdownError) as info:
+        fullsolve.pcg_full(spec, A, P, b, 1e-8, 5)
+    assert info.value.iteration == 1
+
+
+def test_zero_rhs():
+    n = 15
+    spec = fl.laplacian_spectrum(n, 2)
+    A = torch.ones((n, n), dtype=torch.float64, device="cuda")
+    x, rep = fullsolve.pcg_full(spec, A, A, torch.zeros_like(A), 1e-8, 5)
+    assert rep.converged and rep.iterations == 0 and float(x.abs().max()) == 0.0
+
+
+def test_state_full_matches_oracle():
+    n = 31
+    spec = fl.laplacian_spectrum(n, 3)
+    y = np.random.default_rng(0).standard_normal((n, n, n))
+    cfg = fl.SolverConfig(alpha=0.5, beta=2.0, gamma=1e-3)
+    got = fullsolve.solve_state_full(torch.tensor(y, device="cuda"), cfg, spec)
+    core = oracle.dense_core("g4", [oracle.laplacian_eigenvalues(n)] * 3, 0.5, 1.0, 1e-3 / 4.0)
+    assert rel(got, oracle.apply_full(core, y)) <= 1e-12
