@@ -37,7 +37,7 @@ def control_cores(cfg, spectrum, precond="kronecker", seed=0):
     kind = _control_kind(cfg)
     A = dense_core(kind, spectrum)
     if precond == "kronecker":
-        pre = build_preconditioner(kind, spectrum, cfg.precond_rank, seed=seed)
+        pre = kronecker_preconditioner(cfg, spectrum, seed)
         P = cp_dense(pre.diag.core)
     elif precond == "exact":
         P = dense_core(kind, spectrum, reciprocal=True)
@@ -46,6 +46,16 @@ def control_cores(cfg, spectrum, precond="kronecker", seed=0):
     else:
         raise ValueError("precond must be 'kronecker', 'exact' or 'identity'")
     return A, P
+
+
+def kronecker_preconditioner(cfg, spectrum, seed=0):
+    """The reference's rank-r reciprocal core (solver.py:183-189), built on the
+    device with the dense-level cap lifted to the full grid."""
+    from .decomp import dense_budget
+    kind = _control_kind(cfg)
+    total = int(np.prod(spectrum.mode_sizes, dtype=np.int64))
+    with dense_budget(max(total, 2 ** 24)):
+        return build_preconditioner(kind, spectrum, cfg.precond_rank, seed=seed)
 
 
 def pcg_full(spectrum, A, P, b, tol, k_max, mode="spectral"):
