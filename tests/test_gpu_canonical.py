@@ -148,3 +148,26 @@ def test_solve_control_3d_golden(n3):
     assert rep.converged
     assert abs(rep.iterations - int(g[key + "_iters"])) <= 1
     assert rel(fl.cp_to_dense(u), g[key + "_u"]) <= 1e-6
+
+
+def test_merge_collinear_matches_all_pairs_rule():
+    """The sort-based candidate search finds exactly the reference's all-pairs hits."""
+    from paper_1809_01971_b200.decomp import _collinear_pairs
+    rng = np.random.default_rng(9)
+    dims = (20, 17, 13)
+    base = [rng.standard_normal((n, 40)) for n in dims]
+    # duplicate some terms (with sign flips) and add near-duplicates that must NOT merge
+    cols = list(range(40)) + [3, 7, 7, 21]
+    fs = [B[:, cols].copy() for B in base]
+    fs[0][:, 41] *= -1.0
+    fs[1][:, 42] += 1e-4
+    w = rng.standard_normal(len(cols))
+    an = fl.cp_normalize(fl.CpTensor(w, fs))
+    pairs, signs = _collinear_pairs(an)
+    F = [U.cpu().numpy() for U in an.factors]
+    C = np.ones((len(cols), len(cols)))
+    for U in F:
+        C *= U.T @ U
+    want = np.argwhere(np.triu(np.abs(C) >= 1.0 - 1e-13, k=1))
+    assert pairs.tolist() == want.tolist()
+    assert np.array_equal(signs, np.sign(C[want[:, 0], want[:, 1]]))

@@ -11,6 +11,12 @@ if which == "canon":
     spec = fl.laplacian_spectrum(n, 3)
     y = fl.gaussian_bumps(n, 3, 8, seed=11)
     cfg = fl.SolverConfig(alpha=alpha, beta=1e-2, eps=1e-8, precond_rank=6, residual_tol=1e-6, k_max=60)
+    import paper_1809_01971_b200.decomp as dec
+    orig = dec.trunc
+    def traced(x, spec):
+        out = orig(x, spec); print("  trunc rank %d -> %d" % (x.rank, out.rank)); return out
+    import paper_1809_01971_b200.solver as sol
+    sol.trunc = traced
     pr = cProfile.Profile(); t0 = time.time(); pr.enable()
     u, rep = fl.solve_control(y, cfg, spec)
     torch.cuda.synchronize(); pr.disable()
