@@ -272,6 +272,8 @@ def run_gpu(args):
         te = float(tt)
     e2e = world * N3 * ke / te / 1e9
 
+    solves = None if args.no_solves else run_solves(args, rank, world, dev)
+
     if rank == 0:
         peak, peak_kind = _peaks()
         dom = max(per_kernel.items(), key=lambda kv: kv[1][0])
@@ -306,6 +308,8 @@ def run_gpu(args):
             "gpu_launches": len(passes) * K,
             "clocks": clocks,
         }
+        if solves is not None:
+            line["solves"] = solves
         if world == 1 and not args.no_cpu:
             workers = os.cpu_count() or 1
             cpu_apply_rate(127, workers)
@@ -318,6 +322,93 @@ def run_gpu(args):
     return 0
 
 
+def _dev_time(fn, world):
+    """Run fn() bracketed by barrier + CUDA events; returns (result, max seconds over ranks)."""
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    out = fn()
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / 1e3
+    if world > 1:
+        tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt)
+    return out, t
+
+
+def run_solves(args, rank, world, dev):
+    """PCG control solves of BASELINE configs[0], [1] (rank 0) and [3] (all ranks)."""
+    import numpy as np
+    import torch
+    import paper_1809_01971_b200 as fl
+    from paper_1809_01971_b200 import distributed as D, fullsolve
+    from paper_1809_01971_b200.full import cp_dense
+
+    out = {}
+    if rank == 0:
+        # configs[0]: 2D full-format control solve, n=255, 4 seeded bumps
+        n = 255
+        spec = fl.laplacian_spectrum(n, 2)
+        y = cp_dense(fl.gaussian_bumps(n, 2, 4, seed=2024))
+        cfg = fl.SolverConfig(alpha=0.5, beta=1e-3, eps=1e-10, precond_rank=6, residual_tol=1e-8, k_max=100)
+        warm = fullsolve.control_cores(cfg, spec)  # warm-up (tables, cuSOLVER handles, kernel loads)
+        fullsolve.solve_control_full(y, cfg, spec, cores=warm)
+        cores, t_setup = _dev_time(lambda: fullsolve.control_cores(cfg, spec), 1)
+        (u, rep), t_solve = _dev_time(lambda: fullsolve.solve_control_full(y, cfg, spec, cores=cores), 1)
+        out["config0_2d_full"] = {"n": n, "setup_s": t_setup, "solve_s": t_solve, "iterations": rep.iterations,
+                                  "final_residual": rep.residuals[-1], "path": "spectral PCG, 1 persistent kernel"}
+        # configs[1]: 3D canonical control solve, n=127, alpha=0.5, rank-8 bump target, eps=1e-8
+        n = 127
+        spec = fl.laplacian_spectrum(n, 3)
+        y = fl.gaussian_bumps(n, 3, 8, seed=11)
+        cfg = fl.SolverConfig(alpha=0.5, beta=1e-2, eps=1e-8, precond_rank=6, residual_tol=1e-6, k_max=60)
+        (u, rep), t = _dev_time(lambda: fl.solve_control(y, cfg, spec), 1)
+        out["config1_3d_canonical"] = {"n": n, "alpha": 0.5, "seconds": t, "iterations": rep.iterations,
+                                       "final_rank": u.rank, "final_residual": rep.residuals[-1],
+                                       "path": "canonical PCG, trunc after every step (operator build included)"}
+    # configs[3]: 3D full-format control solve, slab-partitioned over the ranks
+    n = args.solve_n
+    lay = D.SlabLayout((n, n, n), world, rank)
+    spec = fl.laplacian_spectrum(n, 3)
+    cfg = fl.SolverConfig(alpha=0.75, beta=1e-4, precond_rank=6, residual_tol=1e-8, k_max=100)
+    tgt = fl.gaussian_bumps(n, 3, 16, seed=7)
+    xs, xe = lay.X[rank]
+    slab_cp = fl.CpTensor(tgt.weights, [tgt.factors[0][xs:xe], tgt.factors[1], tgt.factors[2]])
+    y = cp_dense(slab_cp) if xe > xs else torch.zeros(lay.nodal_shape, dtype=torch.float64, device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(77 + rank)
+    y.add_(1e-3 * torch.randn(y.shape, dtype=torch.float64, device=dev, generator=gen))
+
+    def setup():
+        pre = fullsolve.kronecker_preconditioner(cfg, spec)
+        kind = fullsolve._control_kind(cfg)
+        return D.spectral_core(kind, spec, lay), D.spectral_cp_core(pre.diag.core, lay)
+
+    (A, P), t_setup = _dev_time(setup, world)
+    ops = D.CudaOps()
+    if world == 1:
+        (u, rep), t_solve = _dev_time(lambda: fullsolve.solve_control_full(y, cfg, spec, cores=(A, P)), 1)
+        its, res = rep.iterations, rep.residuals[-1]
+        path = "spectral PCG, 1 persistent kernel"
+    else:
+        (u, its, hist, conv), t_solve = _dev_time(lambda: D.pcg_slab(y, A, P, lay, ops, cfg.residual_tol, cfg.k_max),
+                                                   world)
+        res = hist[-1]
+        path = "slab-partitioned: NCCL all_to_all transposes + phase kernels with scalar all-reduces"
+    out["config3_3d_slab"] = {"n": n, "n_gpus": world, "setup_s": t_setup, "solve_s": t_solve, "iterations": its,
+                              "final_residual": res, "dof": n ** 3, "path": path}
+    del A, P, y, u
+    torch.cuda.empty_cache()
+    return out if rank == 0 else None
+
+
 def main(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -326,6 +417,8 @@ def main(argv=None):
     p.add_argument("--impl", default="b200", choices=("b200", "reference"))
     p.add_argument("--n", type=int, default=511)
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-solves", action="store_true")
+    p.add_argument("--solve-n", type=int, default=1023)
     args = p.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
