@@ -216,8 +216,24 @@ __device__ __forceinline__ void dit_stage(const Cells<LOGN, NFFT, SWZ>& cs, cons
 #pragma unroll
       for (int t = 0; t < R; ++t) v[t] = row[t * ST * NFFT + (pk ^ swz_key<LOGN, CS::LOGF, SWZ>(t << LGST))];
       if constexpr (LGST > 0) {
-#pragma unroll
-        for (int q = 1; q < R; ++q) v[q] = cmul(v[q], __ldg(&tw[(j * q) << (LOGN - LGL)]));
+        // twiddles before the butterfly: W^j, W^2j, W^4j from the table, the
+        // rest as products (7 table loads in flight next to R points spill)
+        constexpr int SH = LOGN - LGL;
+        const double2 w1 = __ldg(&tw[j << SH]);
+        v[1] = cmul(v[1], w1);
+        if constexpr (R >= 4) {
+          const double2 w2 = __ldg(&tw[(2 * j) << SH]);
+          v[2] = cmul(v[2], w2);
+          const double2 w3 = cmul(w1, w2);
+          v[3] = cmul(v[3], w3);
+          if constexpr (R == 8) {
+            const double2 w4 = __ldg(&tw[(4 * j) << SH]);
+            v[4] = cmul(v[4], w4);
+            v[5] = cmul(v[5], cmul(w1, w4));
+            v[6] = cmul(v[6], cmul(w2, w4));
+            v[7] = cmul(v[7], cmul(w3, w4));
+          }
+        }
       }
       dftR<RL>(v);
 #pragma unroll
@@ -403,6 +419,19 @@ __device__ __forceinline__ double out_elem(const Cells<LOGN, NFFT, SWZ>& cs, int
   return reinterpret_cast<const double*>(cs.D)[2 * Cells<LOGN, NFFT, SWZ>::idx(out_pos<LOGN>(j), l >> 1) + (l & 1)];
 }
 
+// Opaque copy: stops the compiler from carrying values (and everything it
+// derived from them) across phases, which otherwise blows the register file.
+__device__ __forceinline__ int64_t launder(int64_t v) {
+  int64_t r;
+  asm volatile("mov.b64 %0, %1;" : "=l"(r) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ int launder(int v) {
+  int r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+
 // per-tile addressing: element (l, j) (j in [1, n]) at base + l*LS + (j-1)*JS
 struct TileAddr {
   int64_t base;  // element offset of (0, 1)
@@ -410,6 +439,15 @@ struct TileAddr {
   int LS;
   int lmax;  // lines [0, lmax) are valid
   int64_t c0;
+  __device__ __forceinline__ TileAddr fresh() const {
+    TileAddr t;
+    t.base = launder(base);
+    t.JS = launder(JS);
+    t.LS = launder(LS);
+    t.lmax = launder(lmax);
+    t.c0 = launder(c0);
+    return t;
+  }
 };
 
 template <bool CONTIG, int C>
@@ -573,40 +611,49 @@ __device__ __forceinline__ double post_val(const Cells<LOGN, NFFT, SWZ>& cs, int
 
 // fused operator pass, step 1: scale the post-processed forward transform by
 // the core in place (cells perm(k) / perm(N-k) hold rows 2k / 2k+1), with the
-// coalesced store mapping for the core loads.
+// coalesced store mapping for the core loads.  Cells are private to the
+// thread, so no barrier is needed; items go in register batches of 4.
 template <int LOGN, int NFFT, int NT, bool CONTIG>
 __device__ __forceinline__ void dst_core_scale(const DstArgs& a, const Cells<LOGN, NFFT, CONTIG>& cs,
-                                               const TileAddr& ta) {
+                                               const TileAddr& ta_in) {
+  const TileAddr ta = ta_in.fresh();
   using SP = Split<LOGN, NFFT, NT, CONTIG>;
   using CS = Cells<LOGN, NFFT, CONTIG>;
   constexpr int PER = SP::PER;
+  constexpr int B = PER < 4 ? PER : 4;
+  static_assert(PER % B == 0, "batch must divide the per-thread item count");
   int k0, l0;
   SP::base(threadIdx.x, k0, l0);
   const KCells kc = kcells<LOGN>(k0);
   const double* cb = a.core + ta.base + (int64_t)l0 * ta.LS;
-  double ce_v[PER], co_v[PER];
-#pragma unroll
-  for (int it = 0; it < PER; ++it) {
-    const int l = l0 + SP::LD(it);
-    const int k = k0 + SP::MS(it);
-    ce_v[it] = 0.0;
-    co_v[it] = 0.0;
-    if (SP::ok(threadIdx.x, it) && l < ta.lmax) {
-      const double* cl = cb + (int64_t)SP::LD(it) * ta.LS;
-      co_v[it] = __ldg(cl + (int64_t)(2 * k) * ta.JS);
-      if (k > 0) ce_v[it] = __ldg(cl + (int64_t)(2 * k - 1) * ta.JS);
-    }
-  }
   double* D = reinterpret_cast<double*>(cs.D);
 #pragma unroll
-  for (int it = 0; it < PER; ++it) {
-    const int l = l0 + SP::LD(it);
-    if (SP::ok(threadIdx.x, it)) {
-      const int io = 2 * CS::idx(cell_odd<LOGN>(kc, SP::MS(it)), l >> 1) + (l & 1);
-      D[io] *= co_v[it];
-      if (k0 + SP::MS(it) > 0) {
-        const int ie = 2 * CS::idx(cell_even<LOGN>(kc, SP::MS(it)), l >> 1) + (l & 1);
-        D[ie] *= ce_v[it];
+  for (int it0 = 0; it0 < PER; it0 += B) {
+    double ce_v[B], co_v[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int it = it0 + u;
+      const int l = l0 + SP::LD(it);
+      const int k = k0 + SP::MS(it);
+      ce_v[u] = 0.0;
+      co_v[u] = 0.0;
+      if (SP::ok(threadIdx.x, it) && l < ta.lmax) {
+        const double* cl = cb + (int64_t)SP::LD(it) * ta.LS;
+        co_v[u] = __ldg(cl + (int64_t)(2 * k) * ta.JS);
+        if (k > 0) ce_v[u] = __ldg(cl + (int64_t)(2 * k - 1) * ta.JS);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int it = it0 + u;
+      const int l = l0 + SP::LD(it);
+      if (SP::ok(threadIdx.x, it)) {
+        const int io = 2 * CS::idx(cell_odd<LOGN>(kc, SP::MS(it)), l >> 1) + (l & 1);
+        D[io] *= co_v[u];
+        if (k0 + SP::MS(it) > 0) {
+          const int ie = 2 * CS::idx(cell_even<LOGN>(kc, SP::MS(it)), l >> 1) + (l & 1);
+          D[ie] *= ce_v[u];
+        }
       }
     }
   }
@@ -668,12 +715,13 @@ __device__ __forceinline__ void dit_gather_stage(const DstArgs& a, const Cells<L
 // perm(N-k), addresses linear in the unrolled item index.
 template <int LOGN, int NFFT, int NT, bool CONTIG, bool NAT = false>
 __device__ __forceinline__ void dst_store(const DstArgs& a, const Cells<LOGN, NFFT, CONTIG>& cs,
-                                          const TileAddr& ta) {
+                                          const TileAddr& ta_in) {
+  const TileAddr ta = ta_in.fresh();
   using SP = Split<LOGN, NFFT, NT, CONTIG>;
   constexpr int PER = SP::PER;
   const double sc = a.scale;
   int k0, l0;
-  SP::base(threadIdx.x, k0, l0);
+  SP::base(launder((int)threadIdx.x), k0, l0);
   const KCells kc = kcells<LOGN>(k0);
   double* yb = a.y + ta.base + (int64_t)l0 * ta.LS;
 #pragma unroll
@@ -699,20 +747,21 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_fft(const DstArgs a) {
   CS cs{reinterpret_cast<double2*>(smem_dst)};
   double2* scr = reinterpret_cast<double2*>(smem_dst + 2 * (1 << LOGN) * NFFT);
   for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
-    const TileAddr ta = tile_addr<CONTIG, C>(a, tile);
-    dst_load_pre<LOGN, NFFT, NT, CONTIG, LOADER>(a, cs, ta);
+    // per-tile addressing is recomputed (from a laundered tile index) in every
+    // phase that needs it, so nothing address-like stays live across the FFTs
+    dst_load_pre<LOGN, NFFT, NT, CONTIG, LOADER>(a, cs, tile_addr<CONTIG, C>(a, tile));
     __syncthreads();
     fft_rec<LOGN, NFFT, NT, CONTIG, 0, LOGN>(cs, a.tw);
     dst_post<LOGN, NFFT, NT, CONTIG>(cs, scr);
     if constexpr (MIDCORE) {
-      dst_core_scale<LOGN, NFFT, NT, CONTIG>(a, cs, ta);
+      dst_core_scale<LOGN, NFFT, NT, CONTIG>(a, cs, tile_addr<CONTIG, C>(a, launder(tile)));
       __syncthreads();
       dit_gather_stage<LOGN, NFFT, NT, CONTIG>(a, cs);
       dit_rec<LOGN, NFFT, NT, CONTIG, FftPlan<LOGN>::NST - 2>(cs, a.tw);
       dst_post<LOGN, NFFT, NT, CONTIG, true>(cs, scr);
-      dst_store<LOGN, NFFT, NT, CONTIG, true>(a, cs, ta);
+      dst_store<LOGN, NFFT, NT, CONTIG, true>(a, cs, tile_addr<CONTIG, C>(a, launder(tile)));
     } else {
-      dst_store<LOGN, NFFT, NT, CONTIG>(a, cs, ta);
+      dst_store<LOGN, NFFT, NT, CONTIG>(a, cs, tile_addr<CONTIG, C>(a, launder(tile)));
     }
     __syncthreads();
   }
@@ -727,6 +776,8 @@ struct DstShape {
   static constexpr int MINB = LOGN >= 13 ? 1 : (LOGN >= 8 ? 2 : (LOGN <= 5 ? 8 : 4));
   // the fused operator pass stages its whole tile in registers across a
   // barrier: twice the threads halves the per-thread share
+  // the fused pass carries more live state across its two transforms: half
+  // the threads, twice the register budget (128), no spills
   static constexpr int NT_MID = NT;
   static constexpr int MINB_MID = MINB;
   static constexpr size_t smem(int nt) { return size_t(16) * (size_t(1) << LOGN) * NFFT + size_t(16) * NFFT * (nt / 32); }

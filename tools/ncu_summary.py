@@ -18,8 +18,9 @@ for v in vals:
     for k in want:
         if k in d:
             lines.append("%-60s %s %s" % (k, d[k], u.get(k, "")))
-    rd = float(d.get("dram__bytes_read.sum", "0").replace(",", "") or 0)
-    wr = float(d.get("dram__bytes_write.sum", "0").replace(",", "") or 0)
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    rd = float(d.get("dram__bytes_read.sum", "0").replace(",", "") or 0) * scale.get(u.get("dram__bytes_read.sum", "byte"), 1.0)
+    wr = float(d.get("dram__bytes_write.sum", "0").replace(",", "") or 0) * scale.get(u.get("dram__bytes_write.sum", "byte"), 1.0)
     lines.append("%-60s %.6e bytes" % ("traffic (dram read + write)", rd + wr))
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"], capture_output=True, text=True).stdout
 srows = list(csv.reader(io.StringIO(src)))
