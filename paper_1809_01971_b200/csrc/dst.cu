@@ -1,12 +1,14 @@
 // Host side of the DST-I transforms: per-length tables, kernel dispatch,
 // and the dense sine-matrix path for lengths without an FFT plan.
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <vector>
 
 #include "common.cuh"
 #include "dst_fft.cuh"
+#include "dst_warp.cuh"
 #include "kernels.cuh"
 
 namespace fl {
@@ -118,6 +120,16 @@ int get_tables(int64_t n, const Tables** out) {
 
 namespace {
 
+// FL_DST_WARP=1 selects the warp-per-FFT kernel (A/B; slower on B200 at n=511)
+bool warp_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FL_DST_WARP");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 template <typename K>
 int grid_for(K kernel, int nt, size_t smem, int64_t ntiles, int* grid) {
   static std::mutex mu;
@@ -143,7 +155,31 @@ int grid_for(K kernel, int nt, size_t smem, int64_t ntiles, int* grid) {
 }
 
 template <int LOGN, bool CONTIG, int LOADER, bool MID>
+int launch_warp(DstArgs a, cudaStream_t st) {
+  using S = WarpShape<LOGN>;
+  constexpr int C = 2 * S::W;
+  if (CONTIG) {
+    a.ntiles = (a.outer + C - 1) / C;
+    a.nchunks = 1;
+  } else {
+    a.nchunks = (a.inner + C - 1) / C;
+    a.ntiles = a.outer * a.nchunks;
+  }
+  if (a.ntiles == 0) return FL_OK;
+  auto kern = k_dst_warp<LOGN, S::W, S::MINB, CONTIG, LOADER, MID>;
+  int grid = 0;
+  int rc = grid_for(kern, 32 * S::W, S::SMEM, a.ntiles, &grid);
+  if (rc) return rc;
+  kern<<<grid, 32 * S::W, S::SMEM, st>>>(a);
+  FL_LAUNCH_CHECK();
+  return FL_OK;
+}
+
+template <int LOGN, bool CONTIG, int LOADER, bool MID>
 int launch_fft(DstArgs a, cudaStream_t st) {
+  if constexpr (WarpShape<LOGN>::ENABLED) {
+    if (warp_enabled()) return launch_warp<LOGN, CONTIG, LOADER, MID>(a, st);
+  }
   using S = DstShape<LOGN>;
   constexpr int C = 2 * S::NFFT;
   if (CONTIG) {
