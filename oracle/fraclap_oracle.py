@@ -238,3 +238,40 @@ def reciprocal_svd_core(tag, mus, a, cm, cp, r):
     U, s, Vt = np.linalg.svd(G, full_matrices=False)
     k = min(int(r), int(np.count_nonzero(s > 0.0)))
     return (U[:, :k] * s[:k]) @ Vt[:k]
+
+
+# ---------------------------------------------------------------------------
+# dense helpers mirroring the reference's test oracles (tests/oracles.py)
+# ---------------------------------------------------------------------------
+
+def random_cp_dense(dims, rank, seed, scale=1.0):
+    """Seeded random CP tensor as (weights, factors, dense) (tests/oracles.py:68-78)."""
+    rng = np.random.default_rng(seed)
+    weights = scale * rng.standard_normal(rank)
+    factors = [rng.standard_normal((n, rank)) for n in dims]
+    return weights, factors, cp_to_dense(weights, factors)
+
+
+def dense_apply(core, x):
+    """F f(Lambda) F^T x with the dense sine basis, mode by mode (tests/oracles.py:56-65)."""
+    z = np.asarray(x, dtype=float)
+    d = z.ndim
+    for ax in range(d):
+        F = sine_matrix(z.shape[ax])
+        z = np.moveaxis(np.tensordot(F.T, z, axes=(1, ax)), 0, ax)
+    z = core * z
+    for ax in range(d):
+        F = sine_matrix(z.shape[ax])
+        z = np.moveaxis(np.tensordot(F, z, axes=(1, ax)), 0, ax)
+    return z
+
+
+def kkt_dense_solve(y_design, alpha, beta, gamma):
+    """Spectral-space optimality solve (tests/oracles.py:105-124): returns (y, u)."""
+    d = y_design.ndim
+    lams = [laplacian_eigenvalues(n) for n in y_design.shape]
+    rho = rho_grid(lams)
+    z = transform_full(y_design)
+    u = transform_full(z / (beta * rho ** (-alpha) + (gamma / beta) * rho ** alpha))
+    y = transform_full(z / (1.0 + (gamma / beta ** 2) * rho ** (2.0 * alpha)))
+    return y, u
