@@ -37,19 +37,37 @@ def cp_hadamard(a, b):
     return CpTensor(w, fs)
 
 
+def power_core(mus, p, tol, scale=1.0):
+    """Canonical core of scale * rho^p, rho = sum_l mu_l, p real.
+
+    rho^p = rho^k * rho^-(k-p) with the integer k >= 0 chosen so that the sinc
+    exponent e = k - p is >= 0.5 (the sinc node count grows like 1/e^2,
+    fracop.py:293-297); rho^k is the exact polynomial CP of the eigenvalue sum."""
+    k = max(0, int(np.ceil(p + 0.5)))
+    e = k - p
+    if e == 0.0:
+        core = None
+    else:
+        core = _sinc_core(mus, e, _required_sinc_m(e, tol), 0.8, scale=scale)
+    for _ in range(k):
+        s = _sum_core(mus)
+        core = s if core is None else cp_hadamard(core, s)
+    if e == 0.0:
+        core = CpTensor(core.weights * float(scale), core.factors)
+    return core
+
+
 def control_core_expsum(kind, spectrum, tol):
     """Canonical core of g2 = cm rho^-a + cp rho^a (sum-then-power) from sinc sums."""
     if kind.tag != "g2" or kind.aggregation != "sum-then-power":
         raise ValueError("the exponential-sum route covers the g2 control core")
     mus, a = mode_values(kind, spectrum)
-    half = tol / 2.0
-    minus = _sinc_core(mus, a, _required_sinc_m(a, half), 0.8, scale=float(kind.coeff_minus))
-    if a == 1.0:
-        plus = _sum_core(mus, scale=float(kind.coeff_plus))
-    else:
-        s = _sinc_core(mus, 1.0 - a, _required_sinc_m(1.0 - a, half), 0.8, scale=float(kind.coeff_plus))
-        plus = cp_hadamard(_sum_core(mus), s)
-    return trunc(cp_add(minus, plus), TruncationSpec(tolerance=half))
+    # sinc node counts from the reference's empirical error model, with margin:
+    # the model is tuned for exponents in (0, 1]
+    quad = tol / 20.0
+    minus = power_core(mus, -a, quad, scale=float(kind.coeff_minus))
+    plus = power_core(mus, a, quad, scale=float(kind.coeff_plus))
+    return trunc(cp_add(minus, plus), TruncationSpec(tolerance=tol / 2.0))
 
 
 def preconditioner_coarse(kind, spectrum, r, max_level=511):
