@@ -21,7 +21,7 @@ BUILD = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(HERE, "libfraclap_b200.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-O3",
+NVCC_FLAGS = [*os.environ.get("FL_NVCC_EXTRA", "").split(), "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-O3",
               "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC]
 
 
