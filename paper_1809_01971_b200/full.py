@@ -18,7 +18,7 @@ from . import _lib
 from .fracop import CoreFunctionKind, mode_values_device
 from .spectral import EigenSpectrum, transform_axis
 
-__all__ = ["FullOperator", "dense_core", "apply_full", "transform_full", "inner", "norm"]
+__all__ = ["FullOperator", "dense_core", "apply_full", "transform_full", "apply_host_stream", "inner", "norm"]
 
 
 def _shape_check(spectrum, x):
@@ -122,6 +122,50 @@ class FullOperator:
 
     def __call__(self, x, out=None):
         return apply_full(self.spectrum, self.core, x, self.alpha, out)
+
+
+def apply_host_stream(op, host_inputs, host_outputs, device=None):
+    """Apply `op` to a sequence of host (pinned) tensors, writing host outputs.
+
+    Three CUDA streams pipeline the steps: while step i computes, step i+1's
+    input crosses PCIe host->device and step i-1's result crosses
+    device->host (PCIe is full duplex), with two device buffers per side.
+    Returns the list of host outputs (the `host_outputs` tensors, filled)."""
+    if len(host_inputs) != len(host_outputs):
+        raise ValueError("need one output buffer per input")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    shape = tuple(op.dims)
+    h2d, comp, d2h = (torch.cuda.Stream(dev) for _ in range(3))
+    xin = [torch.empty(shape, dtype=torch.float64, device=dev) for _ in range(2)]
+    yout = [torch.empty(shape, dtype=torch.float64, device=dev) for _ in range(2)]
+    loaded = [torch.cuda.Event() for _ in range(2)]
+    done = [torch.cuda.Event() for _ in range(2)]
+    drained = [torch.cuda.Event() for _ in range(2)]
+    consumed = [torch.cuda.Event() for _ in range(2)]
+    cur = torch.cuda.current_stream(dev)
+    for s in (h2d, comp, d2h):
+        s.wait_stream(cur)
+    for i, (xh, yh) in enumerate(zip(host_inputs, host_outputs)):
+        b = i & 1
+        with torch.cuda.stream(h2d):
+            if i >= 2:
+                h2d.wait_event(consumed[b])
+            xin[b].copy_(xh, non_blocking=True)
+            loaded[b].record(h2d)
+        with torch.cuda.stream(comp):
+            comp.wait_event(loaded[b])
+            if i >= 2:
+                comp.wait_event(drained[b])
+            op(xin[b], out=yout[b])
+            consumed[b].record(comp)
+            done[b].record(comp)
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(done[b])
+            yh.copy_(yout[b], non_blocking=True)
+            drained[b].record(d2h)
+    for s in (h2d, comp, d2h):
+        cur.wait_stream(s)
+    return host_outputs
 
 
 def inner(a, b):

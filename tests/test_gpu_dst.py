@@ -70,3 +70,16 @@ def test_apply_full_matches_oracle(d, n, tag):
     want = oracle.apply_full(core_want, x)
     got = op(torch.tensor(x, device="cuda")).cpu().numpy()
     assert rel(got, want) <= 1e-12
+
+
+def test_apply_host_stream_matches_device_apply():
+    n = 63
+    spec = spectral.laplacian_spectrum(n, 3)
+    op = full.FullOperator.from_kind(CoreFunctionKind("g1", 0.5), spec)
+    xs = [torch.randn((n, n, n), dtype=torch.float64).pin_memory() for _ in range(5)]
+    ys = [torch.empty_like(x).pin_memory() for x in xs]
+    full.apply_host_stream(op, xs, ys)
+    torch.cuda.synchronize()
+    for x, y in zip(xs, ys):
+        want = op(x.cuda()).cpu()
+        assert torch.allclose(y, want, rtol=0, atol=1e-12 * float(want.abs().max()))
