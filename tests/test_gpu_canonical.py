@@ -171,3 +171,16 @@ def test_merge_collinear_matches_all_pairs_rule():
     want = np.argwhere(np.triu(np.abs(C) >= 1.0 - 1e-13, k=1))
     assert pairs.tolist() == want.tolist()
     assert np.array_equal(signs, np.sign(C[want[:, 0], want[:, 1]]))
+
+
+def test_cp_norm_dense_route_matches_gram_route():
+    from paper_1809_01971_b200 import tensor as T
+    rng = np.random.default_rng(2)
+    dims = (9, 8, 7)
+    R = 900  # large enough for the dense route
+    w, f = rng.standard_normal(R), [rng.standard_normal((n, R)) for n in dims]
+    a = fl.CpTensor(w, f)
+    assert a.rank * 504 < a.rank * a.rank * 24 // 4
+    want = np.linalg.norm(oracle.cp_to_dense(w, f))
+    assert fl.cp_norm(a) == pytest.approx(want, rel=1e-12)
+    assert np.sqrt(fl.cp_inner(a, a)) == pytest.approx(want, rel=1e-10)

@@ -21,7 +21,7 @@ if which == "canon":
     u, rep = fl.solve_control(y, cfg, spec)
     torch.cuda.synchronize(); pr.disable()
     print("canonical n=%d alpha=%g: %d its, rank %d, %.2fs, per-it %.3fs" % (n, alpha, rep.iterations, u.rank, time.time() - t0, rep.seconds_per_iteration))
-    pstats.Stats(pr).sort_stats("cumulative").print_stats(28)
+    pstats.Stats(pr).sort_stats("tottime").print_stats(22)
 else:
     n = int(sys.argv[2])
     spec = fl.laplacian_spectrum(n, 3)
