@@ -171,17 +171,12 @@ def run_gpu(args):
     y = torch.empty_like(x)
     stream = torch.cuda.current_stream(dev)
     sp = _lib.stream_ptr(stream)
-    core = op.core
-
-    # the five launches of fl_apply_full, issued one by one so that every
-    # kernel of the timed region is bracketed by CUDA events on its stream
-    passes = [
-        ("dst_mode0", lambda: _lib.call("fl_dst1", _lib.ptr(x), _lib.ptr(y), 1, n, n * n, 1.0, sp), 16),
-        ("dst_mode1", lambda: _lib.call("fl_dst1", _lib.ptr(y), _lib.ptr(y), n, n, n, 1.0, sp), 16),
-        ("dst_core_mode2", lambda: _lib.call("fl_dst1_core", _lib.ptr(y), _lib.ptr(y), _lib.ptr(core), n * n, n, 1, 1.0, sp), 24),
-        ("dst_mode1", lambda: _lib.call("fl_dst1", _lib.ptr(y), _lib.ptr(y), n, n, n, 1.0, sp), 16),
-        ("dst_mode0", lambda: _lib.call("fl_dst1", _lib.ptr(y), _lib.ptr(y), 1, n, n * n, op.alpha, sp), 16),
-    ]
+    # the five launches of fl_apply_full_padded (FullOperator on the padded
+    # layout), issued one by one so that every kernel of the timed region is
+    # bracketed by CUDA events on its stream; 16 B/DoF per plain pass (read +
+    # write), 24 B/DoF for the fused pass (+ core read)
+    passes = [(name, (lambda a=a: full.run_pass(a, sp)), 24 if name.startswith("dst_core") else 16)
+              for name, a in op.passes(x, y)]
 
     def step():
         for _, fn, _ in passes:
@@ -193,7 +188,7 @@ def run_gpu(args):
     ref = op(x)
     step()
     torch.cuda.synchronize()
-    assert torch.allclose(y, ref, rtol=0, atol=1e-12 * float(ref.abs().max())), "pass sequence != fl_apply_full"
+    assert torch.allclose(y, ref, rtol=0, atol=1e-12 * float(ref.abs().max())), "pass sequence != FullOperator apply"
 
     K = args.steps
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(passes) + 1)] for _ in range(K)]

@@ -103,6 +103,29 @@ int fl_sinc_factor(double* U, const double* mu, int64_t n, const double* t,
 int fl_apply_full(const double* x, double* y, const double* core, int d,
                   const int64_t* dims, double alpha, void* stream);
 
+/* Same operator on a padded internal layout: the last mode's rows have
+ * pitch `pitch` >= n_last (e.g. 512 for n = 511) so every row starts on a
+ * 128-byte boundary.  core_p is the core in that padded layout; work is a
+ * caller-owned padded buffer (prod(dims[:-1]) * pitch doubles, padding
+ * zero-initialised once).  x and y are dense (unpadded); the first pass
+ * reads x into the padded layout and the last writes y back, so the
+ * intermediate passes run on aligned rows.  All modes must be FFT lengths
+ * (n+1 a power of two).  x == y allowed. */
+int fl_apply_full_padded(const double* x, double* y, const double* core_p, double* work,
+                         int d, const int64_t* dims, int64_t pitch, double alpha,
+                         void* stream);
+
+/* One DST-I pass with explicit layouts (the building block of the two
+ * calls above; exposed for per-pass timing).  contig != 0: `outer` lines,
+ * row j of line L at L*lp + j.  contig == 0: `outer` blocks of `groups`
+ * column groups of `width` columns, element (block o, group g, column c,
+ * row j) at o*os + g*gp + c + j*js.  in_layout / out_layout are int64[4]
+ * {os, js, gp, lp} for x (and core) / y.  core != NULL (contig only) runs
+ * the fused forward-scale-inverse pass.  FFT lengths only. */
+int fl_dst1_pass(const double* x, double* y, const double* core, int64_t n, int contig,
+                 int64_t outer, int64_t groups, int64_t width, const int64_t* in_layout,
+                 const int64_t* out_layout, double scale, void* stream);
+
 /* y = alpha * F x over all d modes (a full spectral transform). */
 int fl_transform_full(const double* x, double* y, int d, const int64_t* dims,
                       double alpha, void* stream);

@@ -116,6 +116,43 @@ int fl_apply_full(const double* x, double* y, const double* core, int d, const i
   return dst_mode(y, y, 1, n0, n1 * n2, alpha, nullptr, st);
 }
 
+int fl_apply_full_padded(const double* x, double* y, const double* core_p, double* work, int d,
+                         const int64_t* dims, int64_t pitch, double alpha, void* stream) {
+  int rc = check_dims(d, dims);
+  if (rc) return rc;
+  FL_ARG_CHECK(core_p != nullptr && work != nullptr, "padded core and work buffer required");
+  for (int l = 0; l < d; ++l)
+    FL_ARG_CHECK(fft_length(dims[l]), "padded apply needs FFT lengths, mode %d has n = %lld", l, (long long)dims[l]);
+  const int64_t nl = dims[d - 1], P = pitch;
+  FL_ARG_CHECK(P >= nl, "pitch %lld below the last mode size %lld", (long long)P, (long long)nl);
+  cudaStream_t st = as_stream(stream);
+  const PassLayout line{0, 1, 0, P};
+  if (d == 2) {
+    const int64_t n0 = dims[0];
+    const PassLayout dense{0, nl, 0, 0}, padded{0, P, 0, 0};
+    if ((rc = dst_pass(x, work, nullptr, n0, false, 1, 1, nl, dense, padded, 1.0, st))) return rc;
+    if ((rc = dst_pass(work, work, core_p, nl, true, n0, 1, 1, line, line, 1.0, st))) return rc;
+    return dst_pass(work, y, nullptr, n0, false, 1, 1, nl, padded, dense, alpha, st);
+  }
+  const int64_t n0 = dims[0], n1 = dims[1];
+  const PassLayout dense0{0, n1 * nl, nl, 0}, padded0{0, n1 * P, P, 0};
+  const PassLayout mid{n1 * P, P, 0, 0};
+  if ((rc = dst_pass(x, work, nullptr, n0, false, 1, n1, nl, dense0, padded0, 1.0, st))) return rc;
+  if ((rc = dst_pass(work, work, nullptr, n1, false, n0, 1, P, mid, mid, 1.0, st))) return rc;
+  if ((rc = dst_pass(work, work, core_p, nl, true, n0 * n1, 1, 1, line, line, 1.0, st))) return rc;
+  if ((rc = dst_pass(work, work, nullptr, n1, false, n0, 1, P, mid, mid, 1.0, st))) return rc;
+  return dst_pass(work, y, nullptr, n0, false, 1, n1, nl, padded0, dense0, alpha, st);
+}
+
+int fl_dst1_pass(const double* x, double* y, const double* core, int64_t n, int contig, int64_t outer,
+                 int64_t groups, int64_t width, const int64_t* in_layout, const int64_t* out_layout, double scale,
+                 void* stream) {
+  FL_ARG_CHECK(in_layout != nullptr && out_layout != nullptr, "layouts required");
+  const PassLayout in{in_layout[0], in_layout[1], in_layout[2], in_layout[3]};
+  const PassLayout out{out_layout[0], out_layout[1], out_layout[2], out_layout[3]};
+  return dst_pass(x, y, core, n, contig != 0, outer, groups, width, in, out, scale, as_stream(stream));
+}
+
 int fl_transform_full(const double* x, double* y, int d, const int64_t* dims, double alpha, void* stream) {
   int rc = check_dims(d, dims);
   if (rc) return rc;

@@ -8,7 +8,6 @@
 
 #include "common.cuh"
 #include "dst_fft.cuh"
-#include "dst_warp.cuh"
 #include "kernels.cuh"
 
 namespace fl {
@@ -120,16 +119,6 @@ int get_tables(int64_t n, const Tables** out) {
 
 namespace {
 
-// FL_DST_WARP=1 selects the warp-per-FFT kernel (A/B; slower on B200 at n=511)
-bool warp_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("FL_DST_WARP");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
-
 template <typename K>
 int grid_for(K kernel, int nt, size_t smem, int64_t ntiles, int* grid) {
   static std::mutex mu;
@@ -155,39 +144,15 @@ int grid_for(K kernel, int nt, size_t smem, int64_t ntiles, int* grid) {
 }
 
 template <int LOGN, bool CONTIG, int LOADER, bool MID>
-int launch_warp(DstArgs a, cudaStream_t st) {
-  using S = WarpShape<LOGN>;
-  constexpr int C = 2 * S::W;
-  if (CONTIG) {
-    a.ntiles = (a.outer + C - 1) / C;
-    a.nchunks = 1;
-  } else {
-    a.nchunks = (a.inner + C - 1) / C;
-    a.ntiles = a.outer * a.nchunks;
-  }
-  if (a.ntiles == 0) return FL_OK;
-  auto kern = k_dst_warp<LOGN, S::W, S::MINB, CONTIG, LOADER, MID>;
-  int grid = 0;
-  int rc = grid_for(kern, 32 * S::W, S::SMEM, a.ntiles, &grid);
-  if (rc) return rc;
-  kern<<<grid, 32 * S::W, S::SMEM, st>>>(a);
-  FL_LAUNCH_CHECK();
-  return FL_OK;
-}
-
-template <int LOGN, bool CONTIG, int LOADER, bool MID>
 int launch_fft(DstArgs a, cudaStream_t st) {
-  if constexpr (WarpShape<LOGN>::ENABLED) {
-    if (warp_enabled()) return launch_warp<LOGN, CONTIG, LOADER, MID>(a, st);
-  }
   using S = DstShape<LOGN>;
   constexpr int C = 2 * S::NFFT;
   if (CONTIG) {
     a.ntiles = (a.outer + C - 1) / C;
     a.nchunks = 1;
   } else {
-    a.nchunks = (a.inner + C - 1) / C;
-    a.ntiles = a.outer * a.nchunks;
+    a.nchunks = (a.wv + C - 1) / C;
+    a.ntiles = a.outer * a.groups * a.nchunks;
   }
   if (a.ntiles == 0) return FL_OK;
   constexpr int NT = MID ? S::NT_MID : S::NT;
@@ -224,6 +189,52 @@ int dispatch_fft(int logn, const DstArgs& a, cudaStream_t st) {
 
 }  // namespace
 
+// One DST-I pass with explicit input/output layouts (see DstArgs).  FFT
+// lengths only; the standard [outer][n][inner] pass is dst_mode below.
+int dst_pass(const double* x, double* y, const double* core, int64_t n, bool contig, int64_t outer, int64_t groups,
+             int64_t wv, const PassLayout& in, const PassLayout& out, double scale, cudaStream_t st) {
+  FL_ARG_CHECK(n >= 1 && outer >= 0 && groups >= 1 && wv >= 0, "bad DST pass shape");
+  FL_ARG_CHECK(fft_len_ok(n), "pass layouts need an FFT length (n+1 a power of two in [4, 8192]), got %lld",
+               (long long)n);
+  FL_ARG_CHECK(contig || (in.js >= wv && out.js >= wv), "strided pass: row stride below the group width");
+  FL_ARG_CHECK(!contig || (in.lp >= n && out.lp >= n && in.lp < (1ll << 31) && out.lp < (1ll << 31)),
+               "contiguous pass: line pitch must be in [n, 2^31)");
+  if (outer == 0 || wv == 0) return FL_OK;
+  const Tables* t = nullptr;
+  int rc = get_tables(n, &t);
+  if (rc) return rc;
+  const int logn = ilog2_exact(n + 1);
+  const double nrm = std::sqrt(2.0 / (double)(n + 1));
+  DstArgs a{};
+  a.x = x;
+  a.y = y;
+  a.outer = outer;
+  a.n = n;
+  a.groups = groups;
+  a.wv = wv;
+  a.in_os = in.os;
+  a.in_js = in.js;
+  a.in_gp = in.gp;
+  a.in_lp = in.lp;
+  a.out_os = out.os;
+  a.out_js = out.js;
+  a.out_gp = out.gp;
+  a.out_lp = out.lp;
+  a.core = core;
+  a.tw = t->tw;
+  a.sn = t->sn;
+  if (core == nullptr) {
+    a.scale = scale * nrm;
+    return contig ? dispatch_fft<true, LOAD_PLAIN, false>(logn, a, st)
+                  : dispatch_fft<false, LOAD_PLAIN, false>(logn, a, st);
+  }
+  FL_ARG_CHECK(contig, "the fused core pass runs on contiguous lines");
+  a.scale = scale * nrm * nrm;
+  return dispatch_fft<true, LOAD_PLAIN, true>(logn, a, st);
+}
+
+bool fft_length(int64_t n) { return fft_len_ok(n); }
+
 // y = scale * F_n x along the middle axis (optionally core-scaled sandwich)
 int dst_mode(const double* x, double* y, int64_t outer, int64_t n, int64_t inner, double scale,
              const double* core, cudaStream_t st) {
@@ -234,34 +245,16 @@ int dst_mode(const double* x, double* y, int64_t outer, int64_t n, int64_t inner
   int rc = get_tables(n, &t);
   if (rc) return rc;
   if (fft_len_ok(n)) {
-    const int logn = ilog2_exact(n + 1);
-    const double nrm = std::sqrt(2.0 / (double)(n + 1));
-    DstArgs a{};
-    a.x = x;
-    a.y = y;
-    a.outer = outer;
-    a.n = n;
-    a.inner = inner;
-    a.core = core;
-    a.tw = t->tw;
-    a.sn = t->sn;
-    const bool contig = (inner == 1);
-    if (core == nullptr) {
-      a.scale = scale * nrm;
-      return contig ? dispatch_fft<true, LOAD_PLAIN, false>(logn, a, st)
-                    : dispatch_fft<false, LOAD_PLAIN, false>(logn, a, st);
+    if (inner == 1) {
+      const PassLayout l{0, 1, 0, n};
+      return dst_pass(x, y, core, n, true, outer, 1, 1, l, l, scale, st);
     }
-    a.scale = scale * nrm * nrm;
-    if (contig) return dispatch_fft<true, LOAD_PLAIN, true>(logn, a, st);
+    const PassLayout l{n * inner, inner, 0, 0};
+    if (core == nullptr) return dst_pass(x, y, nullptr, n, false, outer, 1, inner, l, l, scale, st);
     // strided fused pass is not instantiated: transform, scale, transform
-    a.scale = nrm;
-    rc = dispatch_fft<false, LOAD_PLAIN, false>(logn, a, st);
-    if (rc) return rc;
-    rc = ew_mul(y, core, y, outer * n * inner, 1.0, st);
-    if (rc) return rc;
-    a.x = y;
-    a.scale = scale * nrm;
-    return dispatch_fft<false, LOAD_PLAIN, false>(logn, a, st);
+    if ((rc = dst_pass(x, y, nullptr, n, false, outer, 1, inner, l, l, 1.0, st))) return rc;
+    if ((rc = ew_mul(y, core, y, outer * n * inner, 1.0, st))) return rc;
+    return dst_pass(y, y, nullptr, n, false, outer, 1, inner, l, l, scale, st);
   }
   // dense sine-matrix path: y_o = c * S x_o
   const double nrm = std::sqrt(2.0 / (double)(n + 1));
@@ -304,7 +297,10 @@ int dst_kr(const double* U, const double* Xs, double* out, int64_t n, int64_t R,
     a.y = out;
     a.outer = 1;
     a.n = n;
-    a.inner = R * S;
+    a.groups = 1;
+    a.wv = R * S;
+    a.in_os = a.out_os = n * R * S;
+    a.in_js = a.out_js = R * S;
     a.U = U;
     a.Xs = Xs;
     a.R = R;

@@ -30,11 +30,18 @@ enum { LOAD_PLAIN = 0, LOAD_KR = 1 };
 struct DstArgs {
   const double* x;
   double* y;
-  int64_t outer, n, inner;  // x viewed as [outer][n][inner]
-  int64_t ntiles, nchunks;  // strided: nchunks = ceil(inner / C)
+  int64_t outer, n;  // contiguous: number of lines; strided: outer blocks
+  // strided tiles: column groups of `wv` valid columns (C-column chunks);
+  // element (row j, column c of group g, block o) at o*os + g*gp + c + j*js.
+  // contiguous tiles: line L, row j at L*lp + j.  in_* address x (and the
+  // core), out_* address y: a pass can change the layout (e.g. pad rows).
+  int64_t groups, wv;
+  int64_t in_os, in_js, in_gp, in_lp;
+  int64_t out_os, out_js, out_gp, out_lp;
+  int64_t ntiles, nchunks;
   double scale;             // applied at the final store
   const double* core;       // fused pass: core tensor, same layout as x
-  // LOAD_KR: virtual input Z[j][c] = U[j][c / S] * Xs[j][c % S], inner = R*S
+  // LOAD_KR: virtual input Z[j][c] = U[j][c / S] * Xs[j][c % S], wv = R*S
   const double* U;
   const double* Xs;
   int64_t R, S;
@@ -450,24 +457,28 @@ struct TileAddr {
   }
 };
 
-template <bool CONTIG, int C>
+template <bool CONTIG, int C, bool OUT = false>
 __device__ __forceinline__ TileAddr tile_addr(const DstArgs& a, int64_t tile) {
   TileAddr t;
   if (CONTIG) {
     const int64_t L0 = tile * C;
-    t.base = L0 * a.n;
+    const int64_t lp = OUT ? a.out_lp : a.in_lp;
+    t.base = L0 * lp;
     t.JS = 1;
-    t.LS = (int)a.n;
+    t.LS = (int)lp;
     const int64_t rem = a.outer - L0;
     t.lmax = (int)(rem < C ? rem : C);
     t.c0 = 0;
   } else {
-    const int64_t o = tile / a.nchunks;
-    const int64_t c0 = (tile - o * a.nchunks) * C;
-    t.base = o * a.n * a.inner + c0;
-    t.JS = a.inner;
+    const int64_t per_o = a.groups * a.nchunks;
+    const int64_t o = tile / per_o;
+    const int64_t r = tile - o * per_o;
+    const int64_t g = r / a.nchunks;
+    const int64_t c0 = (r - g * a.nchunks) * C;
+    t.base = o * (OUT ? a.out_os : a.in_os) + g * (OUT ? a.out_gp : a.in_gp) + c0;
+    t.JS = OUT ? a.out_js : a.in_js;
     t.LS = 1;
-    const int64_t rem = a.inner - c0;
+    const int64_t rem = a.wv - c0;
     t.lmax = (int)(rem < C ? rem : C);
     t.c0 = c0;
   }
@@ -759,9 +770,9 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_fft(const DstArgs a) {
       dit_gather_stage<LOGN, NFFT, NT, CONTIG>(a, cs);
       dit_rec<LOGN, NFFT, NT, CONTIG, FftPlan<LOGN>::NST - 2>(cs, a.tw);
       dst_post<LOGN, NFFT, NT, CONTIG, true>(cs, scr);
-      dst_store<LOGN, NFFT, NT, CONTIG, true>(a, cs, tile_addr<CONTIG, C>(a, launder(tile)));
+      dst_store<LOGN, NFFT, NT, CONTIG, true>(a, cs, tile_addr<CONTIG, C, true>(a, launder(tile)));
     } else {
-      dst_store<LOGN, NFFT, NT, CONTIG>(a, cs, tile_addr<CONTIG, C>(a, launder(tile)));
+      dst_store<LOGN, NFFT, NT, CONTIG>(a, cs, tile_addr<CONTIG, C, true>(a, launder(tile)));
     }
     __syncthreads();
   }

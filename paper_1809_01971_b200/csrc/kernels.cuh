@@ -7,6 +7,16 @@ namespace fl {
 
 int prepare(int64_t n);
 
+// one side of a DST pass layout (see DstArgs in dst_fft.cuh)
+struct PassLayout {
+  int64_t os, js, gp, lp;
+};
+
+bool fft_length(int64_t n);
+
+int dst_pass(const double* x, double* y, const double* core, int64_t n, bool contig, int64_t outer, int64_t groups,
+             int64_t wv, const PassLayout& in, const PassLayout& out, double scale, cudaStream_t st);
+
 // y = scale * F x along the middle axis of [outer][n][inner]; with core != nullptr
 // y = scale * F diag(core) F x (core in the layout of x)
 int dst_mode(const double* x, double* y, int64_t outer, int64_t n, int64_t inner, double scale,

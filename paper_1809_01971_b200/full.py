@@ -7,6 +7,8 @@ resident in HBM (evaluated once per operator by fl_core_eval, or expanded
 from a canonical core by fl_cp_to_dense), and every application is one
 fl_apply_full call: per-mode DST-I passes with the last mode's forward
 transform, core scaling and inverse transform fused into one kernel.
+FullOperator additionally pads the last mode's rows to a 128-byte multiple
+(fl_apply_full_padded) so the intermediate passes run on aligned rows.
 """
 
 from __future__ import annotations
@@ -18,7 +20,7 @@ from . import _lib
 from .fracop import CoreFunctionKind, mode_values_device
 from .spectral import EigenSpectrum, transform_axis
 
-__all__ = ["FullOperator", "dense_core", "apply_full", "transform_full", "apply_host_stream", "inner", "norm"]
+__all__ = ["FullOperator", "padded_pitch", "run_pass", "dense_core", "apply_full", "transform_full", "apply_host_stream", "inner", "norm"]
 
 
 def _shape_check(spectrum, x):
@@ -94,34 +96,120 @@ def transform_full(spectrum, x, direction="forward", alpha=1.0, out=None):
     return y
 
 
-class FullOperator:
-    """alpha * F diag(G) F on dense tensors; G resident in HBM."""
+def _fft_length(n):
+    return 4 <= n + 1 <= 8192 and (n + 1) & n == 0
 
-    def __init__(self, spectrum, core, alpha=1.0):
+
+def padded_pitch(n):
+    """Row pitch of the padded internal layout for a last mode of size n:
+    the next multiple of 16 doubles (128 B), e.g. 512 for n = 511."""
+    return (n + 15) // 16 * 16
+
+
+class FullOperator:
+    """alpha * F diag(G) F on dense tensors; G resident in HBM.
+
+    When every mode is an FFT length (n+1 a power of two) and the last mode
+    is not already a multiple of 16, the operator keeps G in a padded
+    layout (last-mode rows of pitch `padded_pitch(n)`, so every row starts
+    on a 128-byte boundary) together with a padded work tensor, and applies
+    through fl_apply_full_padded: the first pass reads x into the padded
+    layout, the last writes y back dense.  `core` is then a view of the
+    valid part.  The work tensor makes one operator single-stream: concurrent
+    applications of the same operator on different streams would race."""
+
+    def __init__(self, spectrum, core, alpha=1.0, padded=None):
         if not isinstance(spectrum, EigenSpectrum):
             raise ValueError("expected an EigenSpectrum")
         if tuple(core.shape) != tuple(spectrum.mode_sizes):
             raise ValueError("core dims do not match the spectrum")
         self.spectrum = spectrum
-        self.core = core.contiguous()
         self.alpha = float(alpha)
+        dims = tuple(spectrum.mode_sizes)
+        can_pad = spectrum.all_sine and len(dims) in (2, 3) and all(_fft_length(n) for n in dims)
+        if padded is None:
+            padded = can_pad and dims[-1] % 16 != 0
+        if padded and not can_pad:
+            raise ValueError("the padded layout needs sine modes of FFT length")
+        self.pitch = padded_pitch(dims[-1]) if padded else None
+        if padded:
+            pshape = dims[:-1] + (self.pitch,)
+            self.core_p = torch.zeros(pshape, dtype=torch.float64, device=core.device)
+            self.core_p[..., :dims[-1]].copy_(core)
+            self.work = torch.zeros(pshape, dtype=torch.float64, device=core.device)
+            self._core = None
+        else:
+            self.core_p = self.work = None
+            self._core = core.contiguous()
         for m in spectrum.modes:
             _lib.call("fl_prepare", m.n)
 
     @classmethod
-    def from_kind(cls, kind, spectrum, reciprocal=False, device=None):
-        return cls(spectrum, dense_core(kind, spectrum, reciprocal, device))
+    def from_kind(cls, kind, spectrum, reciprocal=False, device=None, padded=None):
+        return cls(spectrum, dense_core(kind, spectrum, reciprocal, device), padded=padded)
 
     @classmethod
-    def from_cp(cls, spectrum, cp):
-        return cls(spectrum, cp_dense(cp))
+    def from_cp(cls, spectrum, cp, padded=None):
+        return cls(spectrum, cp_dense(cp), padded=padded)
 
     @property
     def dims(self):
         return self.spectrum.mode_sizes
 
+    @property
+    def padded(self):
+        return self.pitch is not None
+
+    @property
+    def core(self):
+        """The dense core G (a view of the padded storage when padded)."""
+        if self._core is not None:
+            return self._core
+        return self.core_p[..., :self.dims[-1]]
+
     def __call__(self, x, out=None):
-        return apply_full(self.spectrum, self.core, x, self.alpha, out)
+        if not self.padded:
+            return apply_full(self.spectrum, self._core, x, self.alpha, out)
+        _check_operand(x)
+        _shape_check(self.spectrum, x)
+        if x.device != self.work.device:
+            raise ValueError("operand on %s, operator on %s" % (x.device, self.work.device))
+        y = out if out is not None else torch.empty_like(x)
+        _lib.call("fl_apply_full_padded", _lib.ptr(x), _lib.ptr(y), _lib.ptr(self.core_p), _lib.ptr(self.work),
+                  len(self.dims), _lib.dims_arr(self.dims), self.pitch, self.alpha, _lib.stream_ptr())
+        return y
+
+    def passes(self, x, y):
+        """The DST passes of one application as (name, fl_dst1_pass args)
+        tuples, in launch order (for per-pass timing; same launches as
+        __call__ on a padded operator)."""
+        if not self.padded:
+            raise ValueError("per-pass list is defined for the padded layout")
+        dims, P = tuple(self.dims), self.pitch
+        nl = dims[-1]
+        xp, yp, cp, wp = _lib.ptr(x), _lib.ptr(y), _lib.ptr(self.core_p), _lib.ptr(self.work)
+        if len(dims) == 2:
+            n0 = dims[0]
+            dense, pad, line = (0, nl, 0, 0), (0, P, 0, 0), (0, 1, 0, P)
+            return [("dst_mode0", (xp, wp, None, n0, 0, 1, 1, nl, dense, pad, 1.0)),
+                    ("dst_core_mode1", (wp, wp, cp, nl, 1, n0, 1, 1, line, line, 1.0)),
+                    ("dst_mode0", (wp, yp, None, n0, 0, 1, 1, nl, pad, dense, self.alpha))]
+        n0, n1 = dims[0], dims[1]
+        dense0, pad0 = (0, n1 * nl, nl, 0), (0, n1 * P, P, 0)
+        mid, line = (n1 * P, P, 0, 0), (0, 1, 0, P)
+        return [("dst_mode0", (xp, wp, None, n0, 0, 1, n1, nl, dense0, pad0, 1.0)),
+                ("dst_mode1", (wp, wp, None, n1, 0, n0, 1, P, mid, mid, 1.0)),
+                ("dst_core_mode2", (wp, wp, cp, nl, 1, n0 * n1, 1, 1, line, line, 1.0)),
+                ("dst_mode1", (wp, wp, None, n1, 0, n0, 1, P, mid, mid, 1.0)),
+                ("dst_mode0", (wp, yp, None, n0, 0, 1, n1, nl, pad0, dense0, self.alpha))]
+
+
+def run_pass(args, stream=None):
+    """Launch one fl_dst1_pass from a FullOperator.passes() entry."""
+    x, y, c, n, contig, outer, groups, width, lin, lout, scale = args
+    s = _lib.stream_ptr() if stream is None else stream
+    _lib.call("fl_dst1_pass", x, y, c, n, contig, outer, groups, width, _lib.dims_arr(lin), _lib.dims_arr(lout),
+              float(scale), s)
 
 
 def apply_host_stream(op, host_inputs, host_outputs, device=None):

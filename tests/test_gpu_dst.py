@@ -83,3 +83,106 @@ def test_apply_host_stream_matches_device_apply():
     for x, y in zip(xs, ys):
         want = op(x.cuda()).cpu()
         assert torch.allclose(y, want, rtol=0, atol=1e-12 * float(want.abs().max()))
+
+
+@pytest.mark.parametrize("dims", [(7, 15), (63, 255), (7, 7, 7), (15, 31, 63), (31, 7, 127), (63, 63, 63),
+                                  (3, 127, 255)])
+@pytest.mark.parametrize("tag", ["g1", "g4"])
+def test_apply_full_padded_matches_oracle(dims, tag):
+    """FullOperator on the padded layout (fl_apply_full_padded) vs the oracle
+    and vs the unpadded fl_apply_full on the same core."""
+    alpha = 0.5
+    spec = spectral.EigenSpectrum(tuple(spectral.laplacian_mode(n) for n in dims))
+    kind = CoreFunctionKind(tag, alpha, coeff_minus=1.3, coeff_plus=0.7)
+    lams = [oracle.laplacian_eigenvalues(n) for n in dims]
+    core_want = oracle.dense_core(tag, lams, alpha, 1.3, 0.7)
+    op = full.FullOperator.from_kind(kind, spec, padded=True)
+    assert op.padded and op.pitch == full.padded_pitch(dims[-1]) and op.pitch % 16 == 0
+    assert rel(op.core.cpu().numpy(), core_want) <= 1e-14
+    rng = np.random.default_rng(sum(dims))
+    x = rng.standard_normal(dims)
+    want = oracle.apply_full(core_want, x)
+    xt = torch.tensor(x, device="cuda")
+    got = op(xt)
+    assert rel(got.cpu().numpy(), want) <= 1e-12
+    plain = full.FullOperator(spec, op.core.contiguous(), padded=False)
+    assert not plain.padded
+    assert rel(got.cpu().numpy(), plain(xt).cpu().numpy()) <= 1e-13
+    # in place, and repeated application keeps the padding inert
+    y = xt.clone()
+    op(y, out=y)
+    op(y, out=y)
+    assert rel(y.cpu().numpy(), oracle.apply_full(core_want, want)) <= 1e-12
+    # the per-pass list launches the same computation
+    z = torch.empty_like(xt)
+    for _, a in op.passes(xt, z):
+        full.run_pass(a)
+    assert rel(z.cpu().numpy(), want) <= 1e-12
+
+
+def test_apply_full_padded_big():
+    """n = 511 (the bench size): padded vs unpadded and Parseval-type checks."""
+    n = 511
+    spec = spectral.laplacian_spectrum(n, 3)
+    op = full.FullOperator.from_kind(CoreFunctionKind("g1", 0.5), spec)
+    assert op.padded and op.pitch == 512
+    plain = full.FullOperator(spec, op.core.contiguous(), padded=False)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    x = torch.randn((n, n, n), dtype=torch.float64, device="cuda", generator=g)
+    a = op(x)
+    b = plain(x)
+    assert float(torch.linalg.vector_norm(a - b)) <= 1e-13 * float(torch.linalg.vector_norm(b))
+    # self-adjointness: <Ax, y> = <x, Ay>
+    yv = torch.randn((n, n, n), dtype=torch.float64, device="cuda", generator=g)
+    lhs = float(torch.dot(a.reshape(-1), yv.reshape(-1)))
+    rhs = float(torch.dot(x.reshape(-1), op(yv).reshape(-1)))
+    assert abs(lhs - rhs) <= 1e-11 * abs(lhs)
+
+
+@pytest.mark.parametrize("n", [7, 63, 255])
+def test_dst1_pass_layouts(n):
+    """fl_dst1_pass with distinct input/output layouts vs scipy."""
+    from paper_1809_01971_b200 import _lib
+    rng = np.random.default_rng(n)
+    blocks, groups, width = 2, 3, 5
+    # input: [blocks][n][groups][width] dense; output: [blocks][groups][n][width+3] padded
+    x = rng.standard_normal((blocks, n, groups, width))
+    want = oracle.dst(x, axis=1)
+    xt = torch.tensor(x, device="cuda")
+    yt = torch.full((blocks, groups, n, width + 3), 7.0, dtype=torch.float64, device="cuda")
+    lin = (n * groups * width, groups * width, width, 0)
+    lout = (groups * n * (width + 3), width + 3, n * (width + 3), 0)
+    full.run_pass((_lib.ptr(xt), _lib.ptr(yt), None, n, 0, blocks, groups, width, lin, lout, 2.0))
+    got = yt.cpu().numpy()
+    assert rel(got[..., :width], 2.0 * want.transpose(0, 2, 1, 3)) <= 1e-13
+    assert np.all(got[..., width:] == 7.0)  # padding columns untouched
+    # contiguous lines with pitches, fused core
+    L = 9
+    xl = rng.standard_normal((L, n + 5))
+    core = rng.standard_normal((L, n + 2))
+    xlt = torch.tensor(xl, device="cuda")
+    ct = torch.tensor(core, device="cuda")
+    ylt = torch.zeros((L, n + 1), dtype=torch.float64, device="cuda")
+    full.run_pass((_lib.ptr(xlt), _lib.ptr(ylt), _lib.ptr(ct), n, 1, L, 1, 1, (0, 1, 0, n + 5), (0, 1, 0, n + 1), 1.0))
+    # the core shares the input layout (pitch n+5): core row l starts at l*(n+5)
+    cflat = core.reshape(-1)
+    cl = np.stack([cflat[l * (n + 5): l * (n + 5) + n] for l in range(L)])
+    want_l = oracle.dst(cl * oracle.dst(xl[:, :n], axis=1), axis=1)
+    assert rel(ylt.cpu().numpy()[:, :n], want_l) <= 1e-13
+    assert np.all(ylt.cpu().numpy()[:, n:] == 0.0)
+
+
+def test_padded_errors():
+    from paper_1809_01971_b200 import _lib
+    spec = spectral.laplacian_spectrum(12, 3)  # not an FFT length
+    with pytest.raises(ValueError):
+        full.FullOperator.from_kind(CoreFunctionKind("g1", 0.5), spec, padded=True)
+    assert not full.FullOperator.from_kind(CoreFunctionKind("g1", 0.5), spec).padded
+    x = torch.zeros((15, 15, 15), dtype=torch.float64, device="cuda")
+    w = torch.zeros((15, 15, 16), dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError):
+        _lib.call("fl_apply_full_padded", _lib.ptr(x), _lib.ptr(x), _lib.ptr(w), _lib.ptr(w), 3,
+                  _lib.dims_arr((15, 15, 15)), 14, 1.0, _lib.stream_ptr())
+    with pytest.raises(ValueError):
+        full.run_pass((_lib.ptr(x), _lib.ptr(x), None, 12, 1, 1, 1, 1, (0, 1, 0, 12), (0, 1, 0, 12), 1.0))
