@@ -223,6 +223,11 @@ int dst_pass(const double* x, double* y, const double* core, int64_t n, bool con
   a.core = core;
   a.tw = t->tw;
   a.sn = t->sn;
+  if (!contig && wv % 2 == 0) {
+    auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+    a.vec_in = al(x) && (core == nullptr || al(core)) && in.os % 2 == 0 && in.gp % 2 == 0 && in.js % 2 == 0;
+    a.vec_out = al(y) && out.os % 2 == 0 && out.gp % 2 == 0 && out.js % 2 == 0;
+  }
   if (core == nullptr) {
     a.scale = scale * nrm;
     return contig ? dispatch_fft<true, LOAD_PLAIN, false>(logn, a, st)
@@ -301,6 +306,7 @@ int dst_kr(const double* U, const double* Xs, double* out, int64_t n, int64_t R,
     a.wv = R * S;
     a.in_os = a.out_os = n * R * S;
     a.in_js = a.out_js = R * S;
+    a.vec_out = ((uintptr_t)out & 15) == 0 && (R * S) % 2 == 0;
     a.U = U;
     a.Xs = Xs;
     a.R = R;

@@ -39,6 +39,10 @@ struct DstArgs {
   int64_t in_os, in_js, in_gp, in_lp;
   int64_t out_os, out_js, out_gp, out_lp;
   int64_t ntiles, nchunks;
+  // strided tiles: line pairs (2u, 2u+1) are 16-byte aligned on this side
+  // (even strides and offsets, 16-byte aligned base and core): one vector
+  // access per pair
+  int vec_in, vec_out;
   double scale;             // applied at the final store
   const double* core;       // fused pass: core tensor, same layout as x
   // LOAD_KR: virtual input Z[j][c] = U[j][c / S] * Xs[j][c % S], wv = R*S
@@ -485,12 +489,160 @@ __device__ __forceinline__ TileAddr tile_addr(const DstArgs& a, int64_t tile) {
   return t;
 }
 
-// Work split shared by the load, fused-core and store phases: items (l, k),
+// Work split shared by the load, fused-core and store phases: items (u, k),
+// u a cell column (tile lines 2u and 2u+1, the re/im halves of one packed
+// FFT) and k in [0, H) a row pair; NFFT*H items over NT threads, PER each.
+// Strided tiles: u = t % NFFT fixed, k = t / NFFT + it * (NT / NFFT), so a
+// warp access covers 32/NFFT rows of 2*NFFT consecutive columns.
+// Contiguous tiles: k = t % H (+ multiples of NT when NT < H), u varies.
+template <int LOGN, int NFFT, int NT, bool CONTIG>
+struct Split {
+  static constexpr int N = 1 << LOGN;
+  static constexpr int H = N / 2;
+  static constexpr int ITEMS = NFFT * H;
+  static constexpr int PER = (ITEMS + NT - 1) / NT;
+  // k = k0 + MS(it), u = u0 + LD(it)
+  __device__ __forceinline__ static void base(int t, int& k0, int& u0) {
+    if (CONTIG) {
+      k0 = (NT >= H) ? (t % H) : t;
+      u0 = (NT >= H) ? (t / H) : 0;
+    } else {
+      k0 = t / NFFT;
+      u0 = t % NFFT;
+    }
+  }
+  __host__ __device__ static constexpr int MS(int it) {
+    return CONTIG ? ((NT >= H) ? 0 : (it % (H / NT)) * NT) : it * (NT / NFFT);
+  }
+  __host__ __device__ static constexpr int LD(int it) {
+    return CONTIG ? ((NT >= H) ? it * (NT / H) : it / (H / NT)) : 0;
+  }
+  __device__ __forceinline__ static bool ok(int t, int it) { return ITEMS % NT == 0 || t + it * NT < ITEMS; }
+};
+
+template <int LOADER>
+__device__ __forceinline__ double load_elem(const DstArgs& a, const TileAddr& ta, int l, int row) {
+  if constexpr (LOADER != LOAD_KR) {
+    return __ldg(&a.x[ta.base + (int64_t)l * ta.LS + (int64_t)row * ta.JS]);
+  } else {
+    const int64_t c = ta.c0 + l;
+    const int64_t k = c / a.S, s = c - k * a.S;
+    return __ldg(&a.U[(int64_t)row * a.R + k]) * __ldg(&a.Xs[(int64_t)row * a.S + s]);
+  }
+}
+
+// the pair (lines 2u, 2u+1) at element pointer p: one 16-byte access when
+// the layout keeps pairs aligned (VEC), else two (line 2u+1 may be absent)
+__device__ __forceinline__ double2 ld_pair(const double* p, int64_t ls, bool vec, bool hi) {
+  if (vec) return __ldg(reinterpret_cast<const double2*>(p));
+  return make_double2(__ldg(p), hi ? __ldg(p + ls) : 0.0);
+}
+
+__device__ __forceinline__ void st_pair(double* p, int64_t ls, bool vec, bool hi, double2 v) {
+  if (vec) {
+    *reinterpret_cast<double2*>(p) = v;
+  } else {
+    p[0] = v.x;
+    if (hi) p[ls] = v.y;
+  }
+}
+
+// DST-I pre-processing of rows (j, N-j) of cell column u from pairs (va, vb)
+template <int LOGN, int NFFT, bool SWZ>
+__device__ __forceinline__ void pre_pair(const Cells<LOGN, NFFT, SWZ>& cs, const double* __restrict__ sn, int u, int j,
+                                         double2 va, double2 vb) {
+  constexpr int H = (1 << LOGN) / 2;
+  if (j == H) {
+    cs.st(H, u, make_double2(2.0 * va.x, 2.0 * va.y));
+  } else {
+    const double s = __ldg(&sn[j]);
+    const double sx = s * (va.x + vb.x), dx = 0.5 * (va.x - vb.x);
+    const double sy = s * (va.y + vb.y), dy = 0.5 * (va.y - vb.y);
+    cs.st(j, u, make_double2(sx + dx, sy + dy));
+    cs.st((1 << LOGN) - j, u, make_double2(sx - dx, sy - dy));
+  }
+}
+
+// stage 1: global -> smem with the DST-I pre-processing fused in.  Item
+// (u, k) covers rows j = k + 1 and N - j of lines 2u, 2u+1.  A batch of a
+// thread's loads is issued before any is consumed; addresses advance by
+// per-item constant strides.
+template <int LOGN, int NFFT, int NT, bool CONTIG, int LOADER>
+__device__ __forceinline__ void dst_load_pre(const DstArgs& a, const Cells<LOGN, NFFT, CONTIG>& cs,
+                                             const TileAddr& ta) {
+  using SP = Split<LOGN, NFFT, NT, CONTIG>;
+  constexpr int N = SP::N, H = SP::H, PER = SP::PER;
+  constexpr int B = PER < 4 ? PER : 4;
+  static_assert(PER % B == 0, "batch must divide the per-thread item count");
+  int k0, u0;
+  SP::base(threadIdx.x, k0, u0);
+  if constexpr (LOADER != LOAD_KR) {
+    const bool vec = !CONTIG && a.vec_in;
+    const int64_t LS = ta.LS;
+    const double* xp = a.x + ta.base + (int64_t)(2 * u0) * LS;
+    const double* pa = xp + (int64_t)k0 * ta.JS;            // row j - 1 = k
+    const double* pb = xp + (int64_t)(N - 2 - k0) * ta.JS;  // row N - j - 1
+#pragma unroll
+    for (int it0 = 0; it0 < PER; it0 += B) {
+      double2 xa[B], xb[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int it = it0 + u;
+        const int l = 2 * (u0 + SP::LD(it));
+        const int k = k0 + SP::MS(it);
+        const int64_t lo = (int64_t)(2 * SP::LD(it)) * LS;
+        xa[u] = make_double2(0.0, 0.0);
+        xb[u] = make_double2(0.0, 0.0);
+        if (SP::ok(threadIdx.x, it) && l < ta.lmax) {
+          const bool hi = l + 1 < ta.lmax;
+          xa[u] = ld_pair(pa + lo + (int64_t)SP::MS(it) * ta.JS, LS, vec, hi);
+          if (k + 1 < H) xb[u] = ld_pair(pb + lo - (int64_t)SP::MS(it) * ta.JS, LS, vec, hi);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int it = it0 + u;
+        if (SP::ok(threadIdx.x, it)) pre_pair(cs, a.sn, u0 + SP::LD(it), k0 + SP::MS(it) + 1, xa[u], xb[u]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int it0 = 0; it0 < PER; it0 += B) {
+      double2 xa[B], xb[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int it = it0 + u;
+        const int l = 2 * (u0 + SP::LD(it));
+        const int j = k0 + SP::MS(it) + 1;
+        xa[u] = make_double2(0.0, 0.0);
+        xb[u] = make_double2(0.0, 0.0);
+        if (SP::ok(threadIdx.x, it) && l < ta.lmax) {
+          const bool hi = l + 1 < ta.lmax;
+          xa[u].x = load_elem<LOADER>(a, ta, l, j - 1);
+          if (hi) xa[u].y = load_elem<LOADER>(a, ta, l + 1, j - 1);
+          if (j < H) {
+            xb[u].x = load_elem<LOADER>(a, ta, l, N - j - 1);
+            if (hi) xb[u].y = load_elem<LOADER>(a, ta, l + 1, N - j - 1);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int it = it0 + u;
+        if (SP::ok(threadIdx.x, it)) pre_pair(cs, a.sn, u0 + SP::LD(it), k0 + SP::MS(it) + 1, xa[u], xb[u]);
+      }
+    }
+  }
+  for (int u = threadIdx.x; u < NFFT; u += NT) cs.st(0, u, make_double2(0.0, 0.0));
+}
+
+// Line-based split (strided tiles whose line pairs are not 16-byte aligned):
+// items (l, k),
 // k in [0, H) (a row pair), C*H items over NT threads, PER per thread.
 // Strided tiles: l = t % C fixed, k = t / C + it * (NT / C).
 // Contiguous tiles: k = t % H (+ multiples of NT when NT < H), l varies.
 template <int LOGN, int NFFT, int NT, bool CONTIG>
-struct Split {
+struct SplitL {
   static constexpr int N = 1 << LOGN;
   static constexpr int H = N / 2;
   static constexpr int C = 2 * NFFT;
@@ -518,26 +670,9 @@ struct Split {
   __device__ __forceinline__ static bool ok(int t, int it) { return ITEMS % NT == 0 || t + it * NT < ITEMS; }
 };
 
-template <int LOADER>
-__device__ __forceinline__ double load_elem(const DstArgs& a, const TileAddr& ta, int l, int row) {
-  if constexpr (LOADER == LOAD_PLAIN) {
-    return __ldg(&a.x[ta.base + (int64_t)l * ta.LS + (int64_t)row * ta.JS]);
-  } else {
-    const int64_t c = ta.c0 + l;
-    const int64_t k = c / a.S, s = c - k * a.S;
-    return __ldg(&a.U[(int64_t)row * a.R + k]) * __ldg(&a.Xs[(int64_t)row * a.S + s]);
-  }
-}
-
-// element (l, row j) of the natural-order layout
+// DST-I pre-processing of rows (j, N-j) of one line l from values (va, vb)
 template <int LOGN, int NFFT, bool SWZ>
-__device__ __forceinline__ double& nat(const Cells<LOGN, NFFT, SWZ>& cs, int l, int j) {
-  return cs.re(l, j);
-}
-
-// DST-I pre-processing of rows (j, N-j) from values (va, vb)
-template <int LOGN, int NFFT, bool SWZ>
-__device__ __forceinline__ void pre_pair(const Cells<LOGN, NFFT, SWZ>& cs, const double* __restrict__ sn, int l, int j,
+__device__ __forceinline__ void pre_line(const Cells<LOGN, NFFT, SWZ>& cs, const double* __restrict__ sn, int l, int j,
                                          double va, double vb) {
   constexpr int H = (1 << LOGN) / 2;
   if (j == H) {
@@ -550,19 +685,19 @@ __device__ __forceinline__ void pre_pair(const Cells<LOGN, NFFT, SWZ>& cs, const
   }
 }
 
-// stage 1: global -> smem with the DST-I pre-processing fused in.  Item
-// (l, k) covers rows j = k + 1 and N - j.  All of a thread's loads are issued
+// stage 1 for strided tiles without aligned line pairs: one item per line;
+// item (l, k) covers rows j = k + 1 and N - j.  All of a thread's loads are issued
 // before any is consumed; addresses advance by per-item constant strides.
-template <int LOGN, int NFFT, int NT, bool CONTIG, int LOADER>
-__device__ __forceinline__ void dst_load_pre(const DstArgs& a, const Cells<LOGN, NFFT, CONTIG>& cs,
-                                             const TileAddr& ta) {
-  using SP = Split<LOGN, NFFT, NT, CONTIG>;
+template <int LOGN, int NFFT, int NT>
+__device__ __forceinline__ void dst_load_lines(const DstArgs& a, const Cells<LOGN, NFFT, false>& cs,
+                                               const TileAddr& ta) {
+  using SP = SplitL<LOGN, NFFT, NT, false>;
   constexpr int N = SP::N, H = SP::H, PER = SP::PER;
   constexpr int B = PER < 8 ? PER : 8;
   static_assert(PER % B == 0, "batch must divide the per-thread item count");
   int k0, l0;
   SP::base(threadIdx.x, k0, l0);
-  if constexpr (LOADER == LOAD_PLAIN) {
+  {
     const double* xp = a.x + ta.base + (int64_t)l0 * ta.LS;
     const double* pa = xp + (int64_t)k0 * ta.JS;           // row j - 1 = k
     const double* pb = xp + (int64_t)(N - 2 - k0) * ta.JS; // row N - j - 1
@@ -585,29 +720,7 @@ __device__ __forceinline__ void dst_load_pre(const DstArgs& a, const Cells<LOGN,
 #pragma unroll
       for (int u = 0; u < B; ++u) {
         const int it = it0 + u;
-        if (SP::ok(threadIdx.x, it)) pre_pair(cs, a.sn, l0 + SP::LD(it), k0 + SP::MS(it) + 1, xa[u], xb[u]);
-      }
-    }
-  } else {
-#pragma unroll
-    for (int it0 = 0; it0 < PER; it0 += B) {
-      double xa[B], xb[B];
-#pragma unroll
-      for (int u = 0; u < B; ++u) {
-        const int it = it0 + u;
-        const int l = l0 + SP::LD(it);
-        const int j = k0 + SP::MS(it) + 1;
-        xa[u] = 0.0;
-        xb[u] = 0.0;
-        if (SP::ok(threadIdx.x, it) && l < ta.lmax) {
-          xa[u] = load_elem<LOADER>(a, ta, l, j - 1);
-          if (j < H) xb[u] = load_elem<LOADER>(a, ta, l, N - j - 1);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < B; ++u) {
-        const int it = it0 + u;
-        if (SP::ok(threadIdx.x, it)) pre_pair(cs, a.sn, l0 + SP::LD(it), k0 + SP::MS(it) + 1, xa[u], xb[u]);
+        if (SP::ok(threadIdx.x, it)) pre_line(cs, a.sn, l0 + SP::LD(it), k0 + SP::MS(it) + 1, xa[u], xb[u]);
       }
     }
   }
@@ -622,48 +735,51 @@ __device__ __forceinline__ double post_val(const Cells<LOGN, NFFT, SWZ>& cs, int
 
 // fused operator pass, step 1: scale the post-processed forward transform by
 // the core in place (cells perm(k) / perm(N-k) hold rows 2k / 2k+1), with the
-// coalesced store mapping for the core loads.  Cells are private to the
+// store's item mapping for the core loads.  Cells are private to the
 // thread, so no barrier is needed; items go in register batches of 4.
 template <int LOGN, int NFFT, int NT, bool CONTIG>
 __device__ __forceinline__ void dst_core_scale(const DstArgs& a, const Cells<LOGN, NFFT, CONTIG>& cs,
                                                const TileAddr& ta_in) {
   const TileAddr ta = ta_in.fresh();
   using SP = Split<LOGN, NFFT, NT, CONTIG>;
-  using CS = Cells<LOGN, NFFT, CONTIG>;
   constexpr int PER = SP::PER;
   constexpr int B = PER < 4 ? PER : 4;
   static_assert(PER % B == 0, "batch must divide the per-thread item count");
-  int k0, l0;
-  SP::base(threadIdx.x, k0, l0);
+  int k0, u0;
+  SP::base(threadIdx.x, k0, u0);
   const KCells kc = kcells<LOGN>(k0);
-  const double* cb = a.core + ta.base + (int64_t)l0 * ta.LS;
-  double* D = reinterpret_cast<double*>(cs.D);
+  const bool vec = !CONTIG && a.vec_in;
+  const int64_t LS = ta.LS;
+  const double* cb = a.core + ta.base + (int64_t)(2 * u0) * LS;
 #pragma unroll
   for (int it0 = 0; it0 < PER; it0 += B) {
-    double ce_v[B], co_v[B];
+    double2 ce_v[B], co_v[B];
 #pragma unroll
     for (int u = 0; u < B; ++u) {
       const int it = it0 + u;
-      const int l = l0 + SP::LD(it);
+      const int l = 2 * (u0 + SP::LD(it));
       const int k = k0 + SP::MS(it);
-      ce_v[u] = 0.0;
-      co_v[u] = 0.0;
+      ce_v[u] = make_double2(0.0, 0.0);
+      co_v[u] = make_double2(0.0, 0.0);
       if (SP::ok(threadIdx.x, it) && l < ta.lmax) {
-        const double* cl = cb + (int64_t)SP::LD(it) * ta.LS;
-        co_v[u] = __ldg(cl + (int64_t)(2 * k) * ta.JS);
-        if (k > 0) ce_v[u] = __ldg(cl + (int64_t)(2 * k - 1) * ta.JS);
+        const bool hi = l + 1 < ta.lmax;
+        const double* cl = cb + (int64_t)(2 * SP::LD(it)) * LS;
+        co_v[u] = ld_pair(cl + (int64_t)(2 * k) * ta.JS, LS, vec, hi);
+        if (k > 0) ce_v[u] = ld_pair(cl + (int64_t)(2 * k - 1) * ta.JS, LS, vec, hi);
       }
     }
 #pragma unroll
     for (int u = 0; u < B; ++u) {
       const int it = it0 + u;
-      const int l = l0 + SP::LD(it);
+      const int p = u0 + SP::LD(it);
       if (SP::ok(threadIdx.x, it)) {
-        const int io = 2 * CS::idx(cell_odd<LOGN>(kc, SP::MS(it)), l >> 1) + (l & 1);
-        D[io] *= co_v[u];
+        const int io = cell_odd<LOGN>(kc, SP::MS(it));
+        const double2 vo = cs.ld(io, p);
+        cs.st(io, p, make_double2(vo.x * co_v[u].x, vo.y * co_v[u].y));
         if (k0 + SP::MS(it) > 0) {
-          const int ie = 2 * CS::idx(cell_even<LOGN>(kc, SP::MS(it)), l >> 1) + (l & 1);
-          D[ie] *= ce_v[u];
+          const int ie = cell_even<LOGN>(kc, SP::MS(it));
+          const double2 ve = cs.ld(ie, p);
+          cs.st(ie, p, make_double2(ve.x * ce_v[u].x, ve.y * ce_v[u].y));
         }
       }
     }
@@ -722,13 +838,50 @@ __device__ __forceinline__ void dit_gather_stage(const DstArgs& a, const Cells<L
   __syncthreads();
 }
 
-// store: item (l, k) writes rows 2k (k >= 1) and 2k+1 from cells perm(k) and
-// perm(N-k), addresses linear in the unrolled item index.
+// store: item (u, k) writes rows 2k (k >= 1) and 2k+1 of lines 2u, 2u+1 from
+// cells perm(k) and perm(N-k), addresses linear in the unrolled item index.
 template <int LOGN, int NFFT, int NT, bool CONTIG, bool NAT = false>
 __device__ __forceinline__ void dst_store(const DstArgs& a, const Cells<LOGN, NFFT, CONTIG>& cs,
                                           const TileAddr& ta_in) {
   const TileAddr ta = ta_in.fresh();
   using SP = Split<LOGN, NFFT, NT, CONTIG>;
+  constexpr int PER = SP::PER;
+  const double sc = a.scale;
+  int k0, u0;
+  SP::base(launder((int)threadIdx.x), k0, u0);
+  const KCells kc = kcells<LOGN>(k0);
+  const bool vec = !CONTIG && a.vec_out;
+  const int64_t LS = ta.LS;
+  double* yb = a.y + ta.base + (int64_t)(2 * u0) * LS;
+#pragma unroll
+  for (int it = 0; it < PER; ++it) {
+    const int l = 2 * (u0 + SP::LD(it));
+    const int k = k0 + SP::MS(it);
+    if (SP::ok(threadIdx.x, it) && l < ta.lmax) {
+      const bool hi = l + 1 < ta.lmax;
+      const int p = u0 + SP::LD(it);
+      double* yl = yb + (int64_t)(2 * SP::LD(it)) * LS;
+      const int ce = NAT ? k : cell_even<LOGN>(kc, SP::MS(it));
+      const int co = NAT ? ((SP::N - k) & (SP::N - 1)) : cell_odd<LOGN>(kc, SP::MS(it));
+      // row 2k+1 -> offset 2k, row 2k -> offset 2k-1
+      const double2 vo = cs.ld(co, p);
+      st_pair(yl + (int64_t)(2 * k) * ta.JS, LS, vec, hi, make_double2(sc * vo.x, sc * vo.y));
+      if (k > 0) {
+        const double2 ve = cs.ld(ce, p);
+        st_pair(yl + (int64_t)(2 * k - 1) * ta.JS, LS, vec, hi, make_double2(sc * ve.x, sc * ve.y));
+      }
+    }
+  }
+}
+
+// store for strided tiles without aligned line pairs, one item per line:
+// item (l, k) writes rows 2k (k >= 1) and 2k+1 from cells perm(k) and
+// perm(N-k), addresses linear in the unrolled item index.
+template <int LOGN, int NFFT, int NT>
+__device__ __forceinline__ void dst_store_lines(const DstArgs& a, const Cells<LOGN, NFFT, false>& cs,
+                                                const TileAddr& ta_in) {
+  const TileAddr ta = ta_in.fresh();
+  using SP = SplitL<LOGN, NFFT, NT, false>;
   constexpr int PER = SP::PER;
   const double sc = a.scale;
   int k0, l0;
@@ -741,8 +894,8 @@ __device__ __forceinline__ void dst_store(const DstArgs& a, const Cells<LOGN, NF
     const int k = k0 + SP::MS(it);
     if (SP::ok(threadIdx.x, it) && l < ta.lmax) {
       double* yl = yb + (int64_t)SP::LD(it) * ta.LS;
-      const int ce = NAT ? k : cell_even<LOGN>(kc, SP::MS(it));
-      const int co = NAT ? ((SP::N - k) & (SP::N - 1)) : cell_odd<LOGN>(kc, SP::MS(it));
+      const int ce = cell_even<LOGN>(kc, SP::MS(it));
+      const int co = cell_odd<LOGN>(kc, SP::MS(it));
       // row 2k+1 -> offset 2k, row 2k -> offset 2k-1
       yl[(int64_t)(2 * k) * ta.JS] = sc * post_val(cs, l, co);
       if (k > 0) yl[(int64_t)(2 * k - 1) * ta.JS] = sc * post_val(cs, l, ce);
@@ -760,7 +913,15 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_fft(const DstArgs a) {
   for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
     // per-tile addressing is recomputed (from a laundered tile index) in every
     // phase that needs it, so nothing address-like stays live across the FFTs
-    dst_load_pre<LOGN, NFFT, NT, CONTIG, LOADER>(a, cs, tile_addr<CONTIG, C>(a, tile));
+    if constexpr (!CONTIG && LOADER != LOAD_KR) {
+      if (a.vec_in) {
+        dst_load_pre<LOGN, NFFT, NT, CONTIG, LOADER>(a, cs, tile_addr<CONTIG, C>(a, tile));
+      } else {
+        dst_load_lines<LOGN, NFFT, NT>(a, cs, tile_addr<CONTIG, C>(a, tile));
+      }
+    } else {
+      dst_load_pre<LOGN, NFFT, NT, CONTIG, LOADER>(a, cs, tile_addr<CONTIG, C>(a, tile));
+    }
     __syncthreads();
     fft_rec<LOGN, NFFT, NT, CONTIG, 0, LOGN>(cs, a.tw);
     dst_post<LOGN, NFFT, NT, CONTIG>(cs, scr);
@@ -772,7 +933,15 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_fft(const DstArgs a) {
       dst_post<LOGN, NFFT, NT, CONTIG, true>(cs, scr);
       dst_store<LOGN, NFFT, NT, CONTIG, true>(a, cs, tile_addr<CONTIG, C, true>(a, launder(tile)));
     } else {
-      dst_store<LOGN, NFFT, NT, CONTIG>(a, cs, tile_addr<CONTIG, C, true>(a, launder(tile)));
+      if constexpr (!CONTIG) {
+        if (a.vec_out) {
+          dst_store<LOGN, NFFT, NT, CONTIG>(a, cs, tile_addr<CONTIG, C, true>(a, launder(tile)));
+        } else {
+          dst_store_lines<LOGN, NFFT, NT>(a, cs, tile_addr<CONTIG, C, true>(a, launder(tile)));
+        }
+      } else {
+        dst_store<LOGN, NFFT, NT, CONTIG>(a, cs, tile_addr<CONTIG, C, true>(a, launder(tile)));
+      }
     }
     __syncthreads();
   }
