@@ -157,7 +157,7 @@ int launch_fft(DstArgs a, cudaStream_t st) {
   if (a.ntiles == 0) return FL_OK;
   constexpr int NT = MID ? S::NT_MID : S::NT;
   constexpr int MINB = MID ? S::MINB_MID : S::MINB;
-  constexpr size_t SMEM = S::smem(NT);
+  constexpr size_t SMEM = MID ? S::smem_mid(NT) : S::smem(NT);
   auto kern = k_dst_fft<LOGN, S::NFFT, NT, MINB, CONTIG, LOADER, MID>;
   int grid = 0;
   int rc = grid_for(kern, NT, SMEM, a.ntiles, &grid);

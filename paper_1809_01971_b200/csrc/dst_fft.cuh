@@ -91,6 +91,10 @@ struct Cells {
   __device__ __forceinline__ static int idx(int pos, int p) {
     return pos * NFFT + (p ^ swz_key<LOGN, LOGF, SWZ>(pos));
   }
+  // swizzle key of a position; XOR-linear in pos, so the key of a position
+  // assembled from disjoint bit fields is the XOR of the fields' keys
+  __host__ __device__ static constexpr int key(int pos) { return swz_key<LOGN, LOGF, SWZ>(pos); }
+  __device__ __forceinline__ static int idx_k(int pos, int k, int p) { return pos * NFFT + (p ^ k); }
   __device__ __forceinline__ double2 ld(int pos, int p) const { return D[idx(pos, p)]; }
   __device__ __forceinline__ void st(int pos, int p, double2 v) const { D[idx(pos, p)] = v; }
   __device__ __forceinline__ double& re(int l, int j) const {
@@ -338,29 +342,50 @@ __host__ __device__ constexpr int perm_c(int k) {
 // and, with N - k = ~(k - 1), perm(N - k) = (N-1) - (perm(k0-1) | perm(m*S)).
 struct KCells {
   int pe;   // perm(k0)
-  int po;   // (N-1) - perm(k0-1), unused when k0 == 0
+  int po;   // (N-1) - perm(k0-1) = (N-1) ^ perm(k0-1), unused when k0 == 0
   bool z;   // k0 == 0
+  int ke, ko;  // swizzle keys of pe and po
 };
 
-template <int LOGN>
+// NAT: natural order (cell k holds frequency k), the layout after DIT stages
+template <int LOGN, class CS, bool NAT = false>
 __device__ __forceinline__ KCells kcells(int k0) {
   KCells c;
-  c.pe = perm_of<LOGN>(k0);
+  c.pe = NAT ? k0 : perm_of<LOGN>(k0);
   c.z = (k0 == 0);
-  c.po = (1 << LOGN) - 1 - perm_of<LOGN>(k0 - 1);
+  c.po = (1 << LOGN) - 1 - (NAT ? k0 - 1 : perm_of<LOGN>(k0 - 1));
+  c.ke = CS::key(c.pe);
+  c.ko = CS::key(c.po);
   return c;
 }
 
 // ms is a compile-time constant after loop unrolling; perm_c folds away
-template <int LOGN>
+template <int LOGN, bool NAT = false>
 __device__ __forceinline__ int cell_even(const KCells& c, int ms) {
-  return c.pe | perm_c<LOGN>(ms);
+  return c.pe | (NAT ? ms : perm_c<LOGN>(ms));
 }
 
-template <int LOGN>
+template <int LOGN, bool NAT = false>
 __device__ __forceinline__ int cell_odd(const KCells& c, int ms) {
   constexpr int N = 1 << LOGN;
-  return c.z ? perm_c<LOGN>((N - ms) & (N - 1)) : c.po - perm_c<LOGN>(ms);
+  const int zp = (N - ms) & (N - 1);
+  return c.z ? (NAT ? zp : perm_c<LOGN>(zp)) : c.po ^ (NAT ? ms : perm_c<LOGN>(ms));
+}
+
+// cell indices of the two cells above with the swizzle key assembled from
+// the per-thread keys and compile-time parts
+template <int LOGN, class CS, bool NAT = false>
+__device__ __forceinline__ int even_idx(const KCells& c, int ms, int p) {
+  const int b = NAT ? ms : perm_c<LOGN>(ms);
+  return CS::idx_k(c.pe | b, c.ke ^ CS::key(b), p);
+}
+
+template <int LOGN, class CS, bool NAT = false>
+__device__ __forceinline__ int odd_idx(const KCells& c, int ms, int p) {
+  constexpr int N = 1 << LOGN;
+  const int zp = (N - ms) & (N - 1);
+  const int b = NAT ? ms : perm_c<LOGN>(ms);
+  return c.z ? CS::idx(NAT ? zp : perm_c<LOGN>(zp), p) : CS::idx_k(c.po ^ b, c.ko ^ CS::key(b), p);
 }
 
 // in-place post-process (see header); leaves even outputs in perm(k) and odd
@@ -378,14 +403,25 @@ __device__ __forceinline__ void dst_post(const Cells<LOGN, NFFT, SWZ>& cs, doubl
   // NAT: spectrum in natural order (cell k holds frequency k)
   const int A = NAT ? g * K : perm_of<LOGN>(g * K);
   const int B = (g == 0) ? 0 : (NAT ? N - g * K : (N - 1 - perm_of<LOGN>(g * K - 1)));
+  // cell indices: A and the compile-time parts are disjoint bit fields, so
+  // positions and swizzle keys combine by XOR
+  const int kA = CS::key(A), kB = CS::key(B);
+  constexpr int KN = CS::key(N - 1);
+  auto ck_idx = [&](int i) {
+    const int b = NAT ? i : perm_c<LOGN>(i);
+    return CS::idx_k(A | b, kA ^ CS::key(b), p);
+  };
+  auto cm_idx = [&](int i) {
+    if (i == 0) return CS::idx_k(B, kB, p);
+    const int b = NAT ? i - 1 : perm_c<LOGN>(i - 1);
+    return CS::idx_k((N - 1) ^ A ^ b, KN ^ kA ^ CS::key(b), p);
+  };
   double2 tot = make_double2(0.0, 0.0);
   // P1: split the packed spectra pairwise (k, N-k); R_k summed on the fly
   if (active) {
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-      const int ck_pos = NAT ? A + i : (A | perm_c<LOGN>(i));
-      const int cm_pos = (i == 0) ? B : (NAT ? N - A - i : (N - 1 - (A | perm_c<LOGN>(i - 1))));
-      const int ik = CS::idx(ck_pos, p), im = CS::idx(cm_pos, p);
+      const int ik = ck_idx(i), im = cm_idx(i);
       const double2 ck = cs.D[ik];
       const double2 cm = cs.D[im];
       const double2 e = make_double2(0.5 * (cm.y - ck.y), 0.5 * (ck.x - cm.x));
@@ -407,8 +443,7 @@ __device__ __forceinline__ void dst_post(const Cells<LOGN, NFFT, SWZ>& cs, doubl
   if (active) {
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-      const int cm_pos = (i == 0) ? B : (NAT ? N - A - i : (N - 1 - (A | perm_c<LOGN>(i - 1))));
-      const int im = CS::idx(cm_pos, p);
+      const int im = cm_idx(i);
       const double2 r = cs.D[im];
       run.x += r.x;
       run.y += r.y;
@@ -747,7 +782,7 @@ __device__ __forceinline__ void dst_core_scale(const DstArgs& a, const Cells<LOG
   static_assert(PER % B == 0, "batch must divide the per-thread item count");
   int k0, u0;
   SP::base(threadIdx.x, k0, u0);
-  const KCells kc = kcells<LOGN>(k0);
+  const KCells kc = kcells<LOGN, Cells<LOGN, NFFT, CONTIG>>(k0);
   const bool vec = !CONTIG && a.vec_in;
   const int64_t LS = ta.LS;
   const double* cb = a.core + ta.base + (int64_t)(2 * u0) * LS;
@@ -773,16 +808,56 @@ __device__ __forceinline__ void dst_core_scale(const DstArgs& a, const Cells<LOG
       const int it = it0 + u;
       const int p = u0 + SP::LD(it);
       if (SP::ok(threadIdx.x, it)) {
-        const int io = cell_odd<LOGN>(kc, SP::MS(it));
-        const double2 vo = cs.ld(io, p);
-        cs.st(io, p, make_double2(vo.x * co_v[u].x, vo.y * co_v[u].y));
+        using CS = Cells<LOGN, NFFT, CONTIG>;
+        const int io = odd_idx<LOGN, CS>(kc, SP::MS(it), p);
+        const double2 vo = cs.D[io];
+        cs.D[io] = make_double2(vo.x * co_v[u].x, vo.y * co_v[u].y);
         if (k0 + SP::MS(it) > 0) {
-          const int ie = cell_even<LOGN>(kc, SP::MS(it));
-          const double2 ve = cs.ld(ie, p);
-          cs.st(ie, p, make_double2(ve.x * ce_v[u].x, ve.y * ce_v[u].y));
+          const int ie = even_idx<LOGN, CS>(kc, SP::MS(it), p);
+          const double2 ve = cs.D[ie];
+          cs.D[ie] = make_double2(ve.x * ce_v[u].x, ve.y * ce_v[u].y);
         }
       }
     }
+  }
+}
+
+// Gather table of the fused pass (N <= 1024): entry for DIT-input cell c =
+// the two source cells of y_j, j = perm_inv(c) (rows j and N - j), packed
+// as (pos * NFFT) << 4 | swizzle key, and sin(pi j / N) (0 for j = 0, so
+// that cell gets 0).  Stored t-major (c % R, c / R) so that the lanes of a
+// warp, which share c / R in groups of NFFT, read adjacent entries.
+struct __align__(16) GatherEnt {
+  int ia, ib;
+  double s;
+};
+
+template <int LOGN>
+struct GatherTable {
+  static constexpr bool ON = LOGN <= 10;
+  static constexpr size_t bytes() { return ON ? sizeof(GatherEnt) * (size_t(1) << LOGN) : 0; }
+};
+
+template <int LOGN, int NFFT, int NT, bool SWZ>
+__device__ __forceinline__ void gather_table_fill(const double* __restrict__ sn, GatherEnt* gt) {
+  using CS = Cells<LOGN, NFFT, SWZ>;
+  constexpr int N = 1 << LOGN;
+  constexpr int H = N / 2;
+  constexpr int R = 1 << FftPlan<LOGN>::rlog(FftPlan<LOGN>::NST - 1);
+  for (int c = threadIdx.x; c < N; c += NT) {
+    const int j = perm_inv<LOGN>(c);
+    GatherEnt e;
+    if (j == 0) {
+      e.ia = e.ib = 0;
+      e.s = 0.0;
+    } else {
+      const int pa = out_pos<LOGN>(j);
+      const int pb = (j == H) ? pa : out_pos<LOGN>(N - j);
+      e.ia = ((pa * NFFT) << 4) | CS::key(pa);
+      e.ib = ((pb * NFFT) << 4) | CS::key(pb);
+      e.s = sn[j < H ? j : N - j];
+    }
+    gt[(c % R) * (N / R) + c / R] = e;
   }
 }
 
@@ -793,7 +868,8 @@ __device__ __forceinline__ void dst_core_scale(const DstArgs& a, const Cells<LOG
 // j and N - j, which sit in cells out_pos(j) and out_pos(N - j).  All reads
 // finish before the barrier; each thread then writes its own butterfly.
 template <int LOGN, int NFFT, int NT, bool CONTIG>
-__device__ __forceinline__ void dit_gather_stage(const DstArgs& a, const Cells<LOGN, NFFT, CONTIG>& cs) {
+__device__ __forceinline__ void dit_gather_stage(const DstArgs& a, const Cells<LOGN, NFFT, CONTIG>& cs,
+                                                 const GatherEnt* __restrict__ gt) {
   using CS = Cells<LOGN, NFFT, CONTIG>;
   constexpr int N = 1 << LOGN;
   constexpr int H = N / 2;
@@ -808,6 +884,18 @@ __device__ __forceinline__ void dit_gather_stage(const DstArgs& a, const Cells<L
     if (NB % NT == 0 || b < NB) {
       const int p = b % NFFT;
       const int base = (b / NFFT) * R;
+      if constexpr (GatherTable<LOGN>::ON) {
+        const GatherEnt* e = gt + base / R;
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+          const GatherEnt g = e[t * (N / R)];
+          const double2 xa = cs.D[(g.ia >> 4) + ((g.ia & 15) ^ p)];
+          const double2 xb = cs.D[(g.ib >> 4) + ((g.ib & 15) ^ p)];
+          v[it][t] = make_double2(fma(g.s, xa.x + xb.x, 0.5 * (xa.x - xb.x)), fma(g.s, xa.y + xb.y, 0.5 * (xa.y - xb.y)));
+        }
+        dftR<RL>(v[it]);
+        continue;
+      }
 #pragma unroll
       for (int t = 0; t < R; ++t) {
         const int j = perm_inv<LOGN>(base + t);
@@ -849,7 +937,8 @@ __device__ __forceinline__ void dst_store(const DstArgs& a, const Cells<LOGN, NF
   const double sc = a.scale;
   int k0, u0;
   SP::base(launder((int)threadIdx.x), k0, u0);
-  const KCells kc = kcells<LOGN>(k0);
+  using CS = Cells<LOGN, NFFT, CONTIG>;
+  const KCells kc = kcells<LOGN, CS, NAT>(k0);
   const bool vec = !CONTIG && a.vec_out;
   const int64_t LS = ta.LS;
   double* yb = a.y + ta.base + (int64_t)(2 * u0) * LS;
@@ -861,13 +950,11 @@ __device__ __forceinline__ void dst_store(const DstArgs& a, const Cells<LOGN, NF
       const bool hi = l + 1 < ta.lmax;
       const int p = u0 + SP::LD(it);
       double* yl = yb + (int64_t)(2 * SP::LD(it)) * LS;
-      const int ce = NAT ? k : cell_even<LOGN>(kc, SP::MS(it));
-      const int co = NAT ? ((SP::N - k) & (SP::N - 1)) : cell_odd<LOGN>(kc, SP::MS(it));
       // row 2k+1 -> offset 2k, row 2k -> offset 2k-1
-      const double2 vo = cs.ld(co, p);
+      const double2 vo = cs.D[odd_idx<LOGN, CS, NAT>(kc, SP::MS(it), p)];
       st_pair(yl + (int64_t)(2 * k) * ta.JS, LS, vec, hi, make_double2(sc * vo.x, sc * vo.y));
       if (k > 0) {
-        const double2 ve = cs.ld(ce, p);
+        const double2 ve = cs.D[even_idx<LOGN, CS, NAT>(kc, SP::MS(it), p)];
         st_pair(yl + (int64_t)(2 * k - 1) * ta.JS, LS, vec, hi, make_double2(sc * ve.x, sc * ve.y));
       }
     }
@@ -886,7 +973,7 @@ __device__ __forceinline__ void dst_store_lines(const DstArgs& a, const Cells<LO
   const double sc = a.scale;
   int k0, l0;
   SP::base(launder((int)threadIdx.x), k0, l0);
-  const KCells kc = kcells<LOGN>(k0);
+  const KCells kc = kcells<LOGN, Cells<LOGN, NFFT, false>>(k0);
   double* yb = a.y + ta.base + (int64_t)l0 * ta.LS;
 #pragma unroll
   for (int it = 0; it < PER; ++it) {
@@ -910,6 +997,8 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_fft(const DstArgs a) {
   extern __shared__ __align__(16) double smem_dst[];
   CS cs{reinterpret_cast<double2*>(smem_dst)};
   double2* scr = reinterpret_cast<double2*>(smem_dst + 2 * (1 << LOGN) * NFFT);
+  GatherEnt* gt = reinterpret_cast<GatherEnt*>(smem_dst + 2 * (1 << LOGN) * NFFT + 2 * NFFT * (NT / 32));
+  if constexpr (MIDCORE && GatherTable<LOGN>::ON) gather_table_fill<LOGN, NFFT, NT, CONTIG>(a.sn, gt);
   for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
     // per-tile addressing is recomputed (from a laundered tile index) in every
     // phase that needs it, so nothing address-like stays live across the FFTs
@@ -928,7 +1017,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_fft(const DstArgs a) {
     if constexpr (MIDCORE) {
       dst_core_scale<LOGN, NFFT, NT, CONTIG>(a, cs, tile_addr<CONTIG, C>(a, launder(tile)));
       __syncthreads();
-      dit_gather_stage<LOGN, NFFT, NT, CONTIG>(a, cs);
+      dit_gather_stage<LOGN, NFFT, NT, CONTIG>(a, cs, gt);
       dit_rec<LOGN, NFFT, NT, CONTIG, FftPlan<LOGN>::NST - 2>(cs, a.tw);
       dst_post<LOGN, NFFT, NT, CONTIG, true>(cs, scr);
       dst_store<LOGN, NFFT, NT, CONTIG, true>(a, cs, tile_addr<CONTIG, C, true>(a, launder(tile)));
@@ -961,6 +1050,7 @@ struct DstShape {
   static constexpr int NT_MID = NT;
   static constexpr int MINB_MID = MINB;
   static constexpr size_t smem(int nt) { return size_t(16) * (size_t(1) << LOGN) * NFFT + size_t(16) * NFFT * (nt / 32); }
+  static constexpr size_t smem_mid(int nt) { return smem(nt) + GatherTable<LOGN>::bytes(); }
 };
 
 }  // namespace fl

@@ -14,4 +14,4 @@ for r in rows:
         out.append((ins, st, cur_file, r[0], r[1].strip()[:100]))
 T = sum(o[0] for o in out); S = sum(o[1] for o in out)
 print("by instructions:")
-for o in sorted(out, reverse=True)[:30]: print(f"  {100*o[0]/T:5.1f}% ins {100*o[1]/S:5.1f}% stall  {o[2]}:{o[3]}  {o[4]}")
+for o in sorted(out, reverse=True)[:int(sys.argv[2]) if len(sys.argv) > 2 else 30]: print(f"  {100*o[0]/T:5.1f}% ins {100*o[1]/S:5.1f}% stall  {o[2]}:{o[3]}  {o[4]}")
