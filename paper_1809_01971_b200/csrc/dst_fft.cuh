@@ -312,15 +312,44 @@ __device__ __forceinline__ double2 rank_excl_scan(double2 v, double2* scr) {
     // warp totals per p live in the last NFFT lanes
     if (lane >= 32 - NFFT) scr[warp * NFFT + (lane & (NFFT - 1))] = x;
     __syncthreads();
-    const int p = threadIdx.x & (NFFT - 1);
-    double ox = 0.0, oy = 0.0;
-    for (int w = 0; w < warp; ++w) {
-      const double2 s = scr[w * NFFT + p];
-      ox += s.x;
-      oy += s.y;
+    // warp 0 scans the NW totals of every p in place: lane (p, q) owns a run
+    // of WPL consecutive warps, runs are combined with shuffles over q
+    if (warp == 0) {
+      constexpr int LPP = 32 / NFFT;
+      constexpr int WPL = (PS::NW + LPP - 1) / LPP;
+      const int p = lane & (NFFT - 1), q = lane / NFFT;
+      double2 loc[WPL];
+      double2 sum = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int i = 0; i < WPL; ++i) {
+        const int w = q * WPL + i;
+        loc[i] = (w < PS::NW) ? scr[w * NFFT + p] : make_double2(0.0, 0.0);
+        sum.x += loc[i].x;
+        sum.y += loc[i].y;
+      }
+      double2 inc = sum;
+#pragma unroll
+      for (int d = NFFT; d < 32; d <<= 1) {
+        const double yx = __shfl_up_sync(0xffffffffu, inc.x, d);
+        const double yy = __shfl_up_sync(0xffffffffu, inc.y, d);
+        if (lane >= d) {
+          inc.x += yx;
+          inc.y += yy;
+        }
+      }
+      double2 run = make_double2(inc.x - sum.x, inc.y - sum.y);
+#pragma unroll
+      for (int i = 0; i < WPL; ++i) {
+        const int w = q * WPL + i;
+        if (w < PS::NW) scr[w * NFFT + p] = run;
+        run.x += loc[i].x;
+        run.y += loc[i].y;
+      }
     }
     __syncthreads();
-    return make_double2(x.x - v.x + ox, x.y - v.y + oy);
+    // scr is next written by the following post-process, after its barriers
+    const double2 o = scr[warp * NFFT + (threadIdx.x & (NFFT - 1))];
+    return make_double2(x.x - v.x + o.x, x.y - v.y + o.y);
   }
 }
 
