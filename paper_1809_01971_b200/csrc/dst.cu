@@ -155,6 +155,11 @@ int launch_fft(DstArgs a, cudaStream_t st) {
     a.ntiles = a.outer * a.groups * a.nchunks;
   }
   if (a.ntiles == 0) return FL_OK;
+  FL_ARG_CHECK(a.ntiles < (int64_t(1) << 31), "too many DST tiles (%lld)", (long long)a.ntiles);
+  if (!CONTIG) {
+    a.div_blk = make_fastdiv((uint32_t)(a.groups * a.nchunks));
+    a.div_chunk = make_fastdiv((uint32_t)a.nchunks);
+  }
   constexpr int NT = MID ? S::NT_MID : S::NT;
   constexpr int MINB = MID ? S::MINB_MID : S::MINB;
   constexpr size_t SMEM = MID ? S::smem_mid(NT) : S::smem(NT);

@@ -27,6 +27,23 @@ namespace fl {
 
 enum { LOAD_PLAIN = 0, LOAD_KR = 1 };
 
+// n / d for 0 <= n < 2^31 without a division: q = (umulhi(n, m) + n) >> s
+// with s = ceil(log2 d), m = floor(2^32 (2^s - d) / d) + 1 (set on the host)
+struct FastDiv {
+  uint32_t d, m, s;
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, m) + n) >> s; }
+};
+
+inline FastDiv make_fastdiv(uint32_t d) {
+  uint32_t s = 0;
+  while ((1ull << s) < d) ++s;
+  FastDiv f;
+  f.d = d;
+  f.s = s;
+  f.m = (uint32_t)((((1ull << s) - d) << 32) / d + 1);
+  return f;
+}
+
 struct DstArgs {
   const double* x;
   double* y;
@@ -39,6 +56,7 @@ struct DstArgs {
   int64_t in_os, in_js, in_gp, in_lp;
   int64_t out_os, out_js, out_gp, out_lp;
   int64_t ntiles, nchunks;
+  FastDiv div_blk, div_chunk;  // strided tiles: by groups*nchunks and by nchunks
   // strided tiles: line pairs (2u, 2u+1) are 16-byte aligned on this side
   // (even strides and offsets, 16-byte aligned base and core): one vector
   // access per pair
@@ -538,12 +556,13 @@ __device__ __forceinline__ TileAddr tile_addr(const DstArgs& a, int64_t tile) {
     t.lmax = (int)(rem < C ? rem : C);
     t.c0 = 0;
   } else {
-    const int64_t per_o = a.groups * a.nchunks;
-    const int64_t o = tile / per_o;
-    const int64_t r = tile - o * per_o;
-    const int64_t g = r / a.nchunks;
-    const int64_t c0 = (r - g * a.nchunks) * C;
-    t.base = o * (OUT ? a.out_os : a.in_os) + g * (OUT ? a.out_gp : a.in_gp) + c0;
+    // tile = (o * groups + g) * nchunks + chunk, ntiles < 2^31
+    const uint32_t t32 = (uint32_t)tile;
+    const uint32_t o = a.div_blk.div(t32);
+    const uint32_t r = t32 - o * a.div_blk.d;
+    const uint32_t g = a.div_chunk.div(r);
+    const int64_t c0 = (int64_t)(r - g * a.div_chunk.d) * C;
+    t.base = (int64_t)o * (OUT ? a.out_os : a.in_os) + (int64_t)g * (OUT ? a.out_gp : a.in_gp) + c0;
     t.JS = OUT ? a.out_js : a.in_js;
     t.LS = 1;
     const int64_t rem = a.wv - c0;
