@@ -14,7 +14,8 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfraclap_b200.so")
+# FL_LIB_OVERRIDE: A/B timing of kernel variants (dev tools only)
+LIB_PATH = os.environ.get("FL_LIB_OVERRIDE") or os.path.join(_HERE, "libfraclap_b200.so")
 
 FL_OK, FL_EINVAL, FL_ECUDA, FL_ENOMEM = 0, 1, 2, 3
 TAGS = ("g1", "g2", "g3", "g4")

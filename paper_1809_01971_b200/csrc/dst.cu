@@ -235,8 +235,10 @@ int dst_pass(const double* x, double* y, const double* core, int64_t n, bool con
   }
   if (core == nullptr) {
     a.scale = scale * nrm;
-    return contig ? dispatch_fft<true, LOAD_PLAIN, false>(logn, a, st)
-                  : dispatch_fft<false, LOAD_PLAIN, false>(logn, a, st);
+    if (contig) return dispatch_fft<true, LOAD_PLAIN, false>(logn, a, st);
+    // scalar line accesses on either side: lighter twiddle loads (measured)
+    return (a.vec_in && a.vec_out) ? dispatch_fft<false, LOAD_PLAIN, false>(logn, a, st)
+                                   : dispatch_fft<false, LOAD_PLAIN_TW3, false>(logn, a, st);
   }
   FL_ARG_CHECK(contig, "the fused core pass runs on contiguous lines");
   a.scale = scale * nrm * nrm;

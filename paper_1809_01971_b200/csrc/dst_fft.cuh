@@ -25,7 +25,9 @@
 
 namespace fl {
 
-enum { LOAD_PLAIN = 0, LOAD_KR = 1 };
+// LOAD_PLAIN_TW3: plain loads, DIF twiddles as 3 table loads + products
+// (cheaper on the LSU pipe; pays off when the tile accesses are scalar)
+enum { LOAD_PLAIN = 0, LOAD_KR = 1, LOAD_PLAIN_TW3 = 2 };
 
 // n / d for 0 <= n < 2^31 without a division: q = (umulhi(n, m) + n) >> s
 // with s = ceil(log2 d), m = floor(2^32 (2^s - d) / d) + 1 (set on the host)
@@ -165,7 +167,7 @@ __device__ __forceinline__ void dftR(double2 (&a)[1 << RL]) {
 // one DIF stage: sub-length L = 2^LGL, radix R = 2^RL, stride st = L / R.
 // Point t of butterfly (block, j) sits at base | (t << LGST): the bits of
 // base and t*ST are disjoint, so the swizzle key splits into key(base) ^ K(t).
-template <int LOGN, int NFFT, int NT, bool SWZ, int LGL, int RL>
+template <int LOGN, int NFFT, int NT, bool SWZ, int LGL, int RL, bool TW3>
 __device__ __forceinline__ void fft_stage(const Cells<LOGN, NFFT, SWZ>& cs, const double2* __restrict__ tw) {
   using CS = Cells<LOGN, NFFT, SWZ>;
   constexpr int N = 1 << LOGN;
@@ -188,9 +190,28 @@ __device__ __forceinline__ void fft_stage(const Cells<LOGN, NFFT, SWZ>& cs, cons
 #pragma unroll
       for (int t = 0; t < R; ++t) v[t] = row[t * ST * NFFT + (pk ^ swz_key<LOGN, CS::LOGF, SWZ>(t << LGST))];
       dftR<RL>(v);
-      if constexpr (LGST > 0) {
+      if constexpr (LGST > 0 && !TW3) {
 #pragma unroll
         for (int q = 1; q < R; ++q) v[q] = cmul(v[q], __ldg(&tw[(j * q) << (LOGN - LGL)]));
+      }
+      if constexpr (LGST > 0 && TW3) {
+        // twiddles W^{jq}: W^j, W^2j, W^4j from the table, the rest as products
+        constexpr int SH = LOGN - LGL;
+        const double2 w1 = __ldg(&tw[j << SH]);
+        v[1] = cmul(v[1], w1);
+        if constexpr (R >= 4) {
+          const double2 w2 = __ldg(&tw[(2 * j) << SH]);
+          const double2 w3 = cmul(w1, w2);
+          v[2] = cmul(v[2], w2);
+          v[3] = cmul(v[3], w3);
+          if constexpr (R == 8) {
+            const double2 w4 = __ldg(&tw[(4 * j) << SH]);
+            v[4] = cmul(v[4], w4);
+            v[5] = cmul(v[5], cmul(w1, w4));
+            v[6] = cmul(v[6], cmul(w2, w4));
+            v[7] = cmul(v[7], cmul(w3, w4));
+          }
+        }
       }
 #pragma unroll
       for (int q = 0; q < R; ++q) row[q * ST * NFFT + (pk ^ swz_key<LOGN, CS::LOGF, SWZ>(q << LGST))] = v[q];
@@ -199,12 +220,12 @@ __device__ __forceinline__ void fft_stage(const Cells<LOGN, NFFT, SWZ>& cs, cons
   __syncthreads();
 }
 
-template <int LOGN, int NFFT, int NT, bool SWZ, int S, int LGL>
+template <int LOGN, int NFFT, int NT, bool SWZ, int S, int LGL, bool TW3 = false>
 __device__ __forceinline__ void fft_rec(const Cells<LOGN, NFFT, SWZ>& cs, const double2* __restrict__ tw) {
   if constexpr (S < FftPlan<LOGN>::NST) {
     constexpr int RL = FftPlan<LOGN>::rlog(S);
-    fft_stage<LOGN, NFFT, NT, SWZ, LGL, RL>(cs, tw);
-    fft_rec<LOGN, NFFT, NT, SWZ, S + 1, LGL - RL>(cs, tw);
+    fft_stage<LOGN, NFFT, NT, SWZ, LGL, RL, TW3>(cs, tw);
+    fft_rec<LOGN, NFFT, NT, SWZ, S + 1, LGL - RL, TW3>(cs, tw);
   }
 }
 
@@ -1060,7 +1081,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_fft(const DstArgs a) {
       dst_load_pre<LOGN, NFFT, NT, CONTIG, LOADER>(a, cs, tile_addr<CONTIG, C>(a, tile));
     }
     __syncthreads();
-    fft_rec<LOGN, NFFT, NT, CONTIG, 0, LOGN>(cs, a.tw);
+    fft_rec<LOGN, NFFT, NT, CONTIG, 0, LOGN, LOADER == LOAD_PLAIN_TW3>(cs, a.tw);
     dst_post<LOGN, NFFT, NT, CONTIG>(cs, scr);
     if constexpr (MIDCORE) {
       dst_core_scale<LOGN, NFFT, NT, CONTIG>(a, cs, tile_addr<CONTIG, C>(a, launder(tile)));
