@@ -17,8 +17,12 @@
 //      tensor and runs steps 1-3 again before storing.
 // Shared-memory layout: complex cells [pos][p], p (FFT index in the tile)
 // fastest.  Contiguous-line tiles (which are transposed on load) XOR-swizzle
-// p by a fold of pos; the fold is XOR-linear so butterfly addresses need one
-// XOR-immediate per access.
+// p by key(pos) = low chunk of pos ^ the chunk holding k's low digit after
+// digit reversal; the key is XOR-linear, so a cell address assembled from
+// disjoint bit fields needs one XOR with a compile-time constant.
+// Global access: items are cell columns (line pairs 2p, 2p+1); on strided
+// tiles with 16-byte aligned pairs each item is one 16-byte load/store.
+// The fused pass reads the DIT input through a shared-memory gather table.
 #pragma once
 
 #include "common.cuh"
@@ -99,6 +103,12 @@ __device__ __forceinline__ int perm_of(int k) {
 template <int LOGN, int LOGF, bool SWZ>
 __host__ __device__ constexpr int swz_key(int pos) {
   if (!SWZ || LOGF == 0) return 0;
+  // low chunk XOR the chunk where the digit reversal puts k's low digit:
+  // a window of consecutive natural positions (load phase) and a window of
+  // consecutive k in digit-reversed positions (post/store phases) both see
+  // distinct keys, except where a window straddles a chunk boundary
+  constexpr int S = LOGN - FftPlan<LOGN>::rlog(0);
+  if (S >= LOGF) return (pos ^ (pos >> S)) & ((1 << LOGF) - 1);
   int k = 0;
   for (int sh = 0; sh < LOGN; sh += LOGF) k ^= (pos >> sh);
   return k & ((1 << LOGF) - 1);
