@@ -295,7 +295,9 @@ def run_gpu(args):
             "config": {"workload": "BASELINE configs[2]: 3D full-format operator apply A^-alpha", "n": n,
                        "alpha": ALPHA, "dof_per_rank": N3, "tensor_bytes": 8 * N3,
                        "l2": "inputs (1.07 GB) larger than L2 (126 MB); no flush needed",
-                       "parallelism": "replicas x%d" % world},
+                       "parallelism": "replicas x%d" % world,
+                       "layout": "x, y dense C order; internal work tensor and core with last-mode rows padded to %s doubles"
+                                 % (op.pitch if op.padded else "n (unpadded)")},
             "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": dbpe * N3, "avg_launch_ms": 1e3 * avg,
