@@ -70,9 +70,29 @@ def control_core_expsum(kind, spectrum, tol):
     return trunc(cp_add(minus, plus), TruncationSpec(tolerance=tol / 2.0))
 
 
-def preconditioner_coarse(kind, spectrum, r, max_level=511):
-    """Rank-r reciprocal core from the multigrid ladder stopped at <= max_level,
-    sides interpolated to the fine grid."""
+def _interp_spectral(V, mu, m):
+    """Tucker side V sampled on level m of the ladder -> all n fine indices.
+
+    Level m samples the fine eigenvalues at the decimated indices
+    (fracop._decimate), so the side columns are functions of the mode value
+    mu; they are interpolated piecewise linearly in log(mu) (linear
+    extrapolation below the first sample), not in grid position."""
+    n = mu.shape[0]
+    pos = np.clip(np.rint((np.arange(m) + 1.0) * (n + 1.0) / (m + 1.0)).astype(int) - 1, 0, n - 1)
+    dev = V.device
+    xs = torch.as_tensor(np.log(mu[pos]), dtype=torch.float64, device=dev)
+    xf = torch.as_tensor(np.log(mu), dtype=torch.float64, device=dev)
+    idx = torch.searchsorted(xs, xf).clamp(1, m - 1)
+    x0, x1 = xs[idx - 1], xs[idx]
+    wgt = ((xf - x0) / (x1 - x0))[:, None]
+    return V[idx - 1] * (1.0 - wgt) + V[idx] * wgt
+
+
+def preconditioner_coarse(kind, spectrum, r, max_level=1023, interp="spectral"):
+    """Rank-r reciprocal core from the multigrid ladder stopped at <= max_level
+    (a dense 1023^3 level is 8.6 GB of HBM), sides interpolated to the fine
+    grid ("spectral": in log(mode value), see _interp_spectral; "grid": the
+    ladder's own position-based prolongation)."""
     sampler, sizes = _mg_sampler(kind, spectrum, reciprocal=True)
     levels = [m for m in sizes if m <= max_level] or sizes[:1]
     ranks = (min(int(r) + 2, sizes[0]),) * spectrum.d
@@ -80,12 +100,17 @@ def preconditioner_coarse(kind, spectrum, r, max_level=511):
         tt = multigrid_tucker(sampler, sizes[0], len(levels), ranks)
     n = spectrum.mode_sizes[0]
     if levels[-1] != n:
-        sides = [_complete_columns(_interp_columns(V, n), rk, trusted=False) for V, rk in zip(tt.sides, ranks)]
+        mus, _ = mode_values(kind, spectrum)
+        if interp == "spectral":
+            fine = [_interp_spectral(V, np.asarray(mu), levels[-1]) for V, mu in zip(tt.sides, mus)]
+        else:
+            fine = [_interp_columns(V, n) for V in tt.sides]
+        sides = [_complete_columns(V, rk, trusted=False) for V, rk in zip(fine, ranks)]
         tt = TuckerTensor(tt.core, sides)
     return t2c(tt, TruncationSpec(max_rank=int(r), mode="fixed-rank"))
 
 
-def solve_control_large(y_design, cfg, spectrum, max_level=511):
+def solve_control_large(y_design, cfg, spectrum, max_level=1023):
     """solve_control (solver.py:203-216) with the large-grid core routes."""
     kind = CoreFunctionKind("g2", cfg.alpha, coeff_minus=float(cfg.beta),
                             coeff_plus=float(cfg.gamma) / float(cfg.beta))
@@ -108,7 +133,7 @@ def problem(i, n, seed=2026):
     return y, cfg
 
 
-def solve_batch(n, count, rank=0, world=1, max_level=511):
+def solve_batch(n, count, rank=0, world=1, max_level=1023):
     """Solve problems rank, rank+world, ... of the batch; returns per-problem records."""
     from .spectral import laplacian_spectrum
     spec = laplacian_spectrum(n, 3)
