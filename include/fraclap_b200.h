@@ -145,6 +145,14 @@ int fl_cp_apply_mode(const double* U, const double* Xs, double* out, int64_t n,
 int fl_cp_gram(int d, const int64_t* n, const double* const* A, int64_t Ra,
                const double* const* B, int64_t Rb, double* H, void* stream);
 
+/* Batched thin SVD of small matrices (one-sided Jacobi, one CTA per
+ * matrix): A is batch x m x n row-major; U (batch, m, k), S (batch, k)
+ * descending, Vt (batch, k, n), k = min(m, n).  The slice SVDs of t2c
+ * (decomp.py:468-519).  Requires (max(m,n)*k + k*k + k) doubles <= 200 KiB
+ * (e.g. m = n <= 110). */
+int fl_svd_batched(const double* A, int batch, int m, int n, double* U, double* S,
+                   double* Vt, void* stream);
+
 /* Column norms of an (n, R) matrix (cp_normalize, tensor.py:180-197). */
 int fl_col_norms(const double* U, int64_t n, int64_t R, double* out, void* stream);
 

@@ -105,8 +105,9 @@ int col_norms(const double* U, int64_t n, int64_t R, double* out, cudaStream_t s
 }
 
 // out[c] scaled columns: V[r][c] = U[r][c] / nrm[c] (nrm == 0 -> e_1 column)
-__global__ void k_col_scale(const double* __restrict__ U, const double* __restrict__ nrm, int64_t n, int64_t R,
-                            double* V) {
+// V may alias U (in-place normalisation): every element is read and written
+// by the same thread
+__global__ void k_col_scale(const double* U, const double* __restrict__ nrm, int64_t n, int64_t R, double* V) {
   const int64_t total = n * R;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / R, c = i % R;

@@ -168,6 +168,10 @@ int fl_transform_full(const double* x, double* y, int d, const int64_t* dims, do
   return dst_mode(y, y, 1, n0, n1 * n2, alpha, nullptr, st);
 }
 
+int fl_svd_batched(const double* A, int batch, int m, int n, double* U, double* S, double* Vt, void* stream) {
+  return svd_batched(A, batch, m, n, U, S, Vt, as_stream(stream));
+}
+
 int fl_cp_apply_mode(const double* U, const double* Xs, double* out, int64_t n, int64_t R, int64_t S, double scale,
                      void* stream) {
   return dst_kr(U, Xs, out, n, R, S, scale, as_stream(stream));

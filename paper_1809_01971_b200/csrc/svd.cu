@@ -1,0 +1,168 @@
+// Batched SVD of small dense matrices by one-sided (Hestenes) Jacobi, one CTA
+// per matrix, the matrix and the accumulated right rotations resident in
+// shared memory.  Used by t2c (decomp.py:468-519: one SVD per core slice),
+// where the library's batched routines either loop over the batch (gesvd,
+// gesvdj beyond 32 x 32) or are approximate (gesvda).
+//
+// Columns of W (m x n, m >= n; the transpose is processed when m < n) are
+// orthogonalised pairwise: a round-robin ordering gives n/2 disjoint pairs
+// per round, one warp per pair; a rotation zeroes the pair's inner product.
+// Sweeps repeat until no pair has |a_p . a_q| > tol sqrt(|a_p|^2 |a_q|^2).
+// Then sigma_j = |a_j|, u_j = a_j / sigma_j, V = accumulated rotations;
+// outputs are sorted by decreasing sigma.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace fl {
+
+namespace {
+
+constexpr int SVD_THREADS = 1024;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// players 0..N-1 (N even): round r pairs 0 with pos(0) and pos(k) with
+// pos(N-1-k), pos(i) = 1 + (i + r) mod (N - 1)
+__device__ __forceinline__ void rr_pair(int N, int r, int k, int& p, int& q) {
+  auto pos = [&](int i) { return 1 + (i + r) % (N - 1); };
+  if (k == 0) {
+    p = 0;
+    q = pos(0);
+  } else {
+    p = pos(k);
+    q = pos(N - 1 - k);
+  }
+}
+
+// A: batch of m x n row-major matrices (leading dim n, batch stride m*n).
+// Outputs: U (batch, m, k), S (batch, k), Vt (batch, k, n), k = min(m, n).
+__global__ void __launch_bounds__(SVD_THREADS) k_svd_jacobi(const double* __restrict__ A, int m, int n,
+                                                            double* __restrict__ U, double* __restrict__ S,
+                                                            double* __restrict__ Vt, int max_sweeps) {
+  extern __shared__ double sm_svd[];
+  const bool tr = m < n;
+  const int M = tr ? n : m;  // rows of the working matrix W
+  const int K = tr ? m : n;  // columns of W (= number of singular values)
+  const int N = K + (K & 1);
+  double* W = sm_svd;              // column-major M x K
+  double* V = sm_svd + (size_t)M * K;  // column-major K x K
+  int* flag = reinterpret_cast<int*>(V + (size_t)K * K);
+  const double* Ab = A + (size_t)blockIdx.x * m * n;
+  // load W = A (columns of A) or A^T (rows of A) column-major
+  for (int idx = threadIdx.x; idx < m * n; idx += blockDim.x) {
+    const int i = idx / n, j = idx - i * n;  // A[i][j]
+    if (!tr)
+      W[(size_t)j * M + i] = Ab[idx];
+    else
+      W[(size_t)i * M + j] = Ab[idx];
+  }
+  for (int idx = threadIdx.x; idx < K * K; idx += blockDim.x) V[idx] = (idx / K == idx % K) ? 1.0 : 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const double tol = 1e-15 * (double)M;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    if (threadIdx.x == 0) *flag = 0;
+    __syncthreads();
+    for (int r = 0; r < N - 1; ++r) {
+      for (int k = warp; k < N / 2; k += nwarps) {
+        int p, q;
+        rr_pair(N, r, k, p, q);
+        if (p >= K || q >= K) continue;
+        double* wp = W + (size_t)p * M;
+        double* wq = W + (size_t)q * M;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = lane; i < M; i += 32) {
+          const double x = wp[i], y = wq[i];
+          al = fma(x, x, al);
+          be = fma(y, y, be);
+          ga = fma(x, y, ga);
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (fabs(ga) <= tol * sqrt(al * be) || ga == 0.0) continue;
+        if (lane == 0) *flag = 1;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+        for (int i = lane; i < M; i += 32) {
+          const double x = wp[i], y = wq[i];
+          wp[i] = c * x - s * y;
+          wq[i] = s * x + c * y;
+        }
+        double* vp = V + (size_t)p * K;
+        double* vq = V + (size_t)q * K;
+        for (int i = lane; i < K; i += 32) {
+          const double x = vp[i], y = vq[i];
+          vp[i] = c * x - s * y;
+          vq[i] = s * x + c * y;
+        }
+      }
+      __syncthreads();
+    }
+    const int any = *flag;
+    __syncthreads();
+    if (!any) break;
+  }
+  // singular values = column norms; rank by decreasing sigma (ties by index)
+  double* sig = reinterpret_cast<double*>(flag + 2);
+  for (int j = warp; j < K; j += nwarps) {
+    const double* wj = W + (size_t)j * M;
+    double a = 0.0;
+    for (int i = lane; i < M; i += 32) a = fma(wj[i], wj[i], a);
+    a = warp_sum(a);
+    if (lane == 0) sig[j] = sqrt(a);
+  }
+  __syncthreads();
+  double* Ub = U + (size_t)blockIdx.x * m * K;
+  double* Sb = S + (size_t)blockIdx.x * K;
+  double* Vb = Vt + (size_t)blockIdx.x * K * n;
+  for (int j = warp; j < K; j += nwarps) {
+    const double sj = sig[j];
+    int rank = 0;
+    for (int i = lane; i < K; i += 32) rank += (sig[i] > sj || (sig[i] == sj && i < j)) ? 1 : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+    if (lane == 0) Sb[rank] = sj;
+    const double inv = sj > 0.0 ? 1.0 / sj : 0.0;
+    const double* wj = W + (size_t)j * M;
+    const double* vj = V + (size_t)j * K;
+    if (!tr) {
+      // A = W_final V^T: U[:, rank] = w_j / s_j (m rows), Vt[rank, :] = v_j (n = K)
+      for (int i = lane; i < m; i += 32) Ub[(size_t)i * K + rank] = (sj > 0.0) ? wj[i] * inv : (i == j ? 1.0 : 0.0);
+      for (int i = lane; i < n; i += 32) Vb[(size_t)rank * n + i] = vj[i];
+    } else {
+      // A^T = W V^T -> A = V W^T: U[:, rank] = v_j (m = K rows), Vt[rank, :] = w_j / s_j
+      for (int i = lane; i < m; i += 32) Ub[(size_t)i * K + rank] = vj[i];
+      for (int i = lane; i < n; i += 32) Vb[(size_t)rank * n + i] = (sj > 0.0) ? wj[i] * inv : (i == j ? 1.0 : 0.0);
+    }
+  }
+}
+
+}  // namespace
+
+size_t svd_batched_smem(int m, int n) {
+  const size_t M = m > n ? m : n, K = m < n ? m : n;
+  return sizeof(double) * (M * K + K * K + K) + 2 * sizeof(int);
+}
+
+int svd_batched(const double* A, int batch, int m, int n, double* U, double* S, double* Vt, cudaStream_t st) {
+  FL_ARG_CHECK(batch >= 0 && m >= 1 && n >= 1, "bad batched SVD shape (%d, %d, %d)", batch, m, n);
+  const size_t smem = svd_batched_smem(m, n);
+  FL_ARG_CHECK(smem <= 200 * 1024, "batched SVD: %d x %d matrices exceed the shared-memory budget", m, n);
+  if (batch == 0) return FL_OK;
+  static bool attr_set = false;
+  if (!attr_set) {
+    FL_CUDA_TRY(cudaFuncSetAttribute(k_svd_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr_set = true;
+  }
+  k_svd_jacobi<<<batch, SVD_THREADS, smem, st>>>(A, m, n, U, S, Vt, 40);
+  FL_LAUNCH_CHECK();
+  return FL_OK;
+}
+
+}  // namespace fl

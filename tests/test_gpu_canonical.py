@@ -222,3 +222,33 @@ def test_trunc_range_compression_matches_uncompressed(dims, R, tol, monkeypatch)
     assert diff <= 1e-3 * tol * dx
     err = fl.cp_norm(fl.cp_add(fast, fl.cp_scale(x, -1.0)))
     assert err <= tol * dx
+
+
+@pytest.mark.parametrize("b,m,n", [(5, 7, 7), (64, 64, 64), (3, 40, 17), (4, 17, 40), (2, 96, 96), (1, 1, 5),
+                                   (0, 8, 8)])
+def test_svd_batched_matches_numpy(b, m, n):
+    from paper_1809_01971_b200.decomp import svd_batched
+    rng = np.random.default_rng(m * n + b)
+    A = rng.standard_normal((b, m, n))
+    if b > 1:  # a rank-deficient slice with a repeated singular value
+        A[1] = 0.0
+        k = min(m, n)
+        if k >= 3:
+            Q1, _ = np.linalg.qr(rng.standard_normal((m, 3)))
+            Q2, _ = np.linalg.qr(rng.standard_normal((n, 3)))
+            A[1] = Q1 @ np.diag([2.0, 2.0, 1e-9]) @ Q2.T
+    At = torch.tensor(A, device="cuda")
+    U, S, Vt = svd_batched(At)
+    U, S, Vt = U.cpu().numpy(), S.cpu().numpy(), Vt.cpu().numpy()
+    k = min(m, n)
+    assert U.shape == (b, m, k) and S.shape == (b, k) and Vt.shape == (b, k, n)
+    for i in range(b):
+        s_ref = np.linalg.svd(A[i], compute_uv=False)
+        assert np.allclose(S[i], s_ref, rtol=0, atol=1e-13 * max(s_ref[0], 1.0))
+        assert np.all(np.diff(S[i]) <= 0.0)
+        keep = S[i] > 1e-12 * max(S[i][0], 1e-300)
+        rec = (U[i][:, keep] * S[i][keep]) @ Vt[i][keep]
+        assert np.linalg.norm(rec - A[i]) <= 1e-13 * max(np.linalg.norm(A[i]), 1.0)
+        Uk, Vk = U[i][:, keep], Vt[i][keep]
+        assert np.allclose(Uk.T @ Uk, np.eye(keep.sum()), atol=1e-12)
+        assert np.allclose(Vk @ Vk.T, np.eye(keep.sum()), atol=1e-12)

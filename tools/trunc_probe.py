@@ -1,6 +1,7 @@
 """Where the time of a configs[4]-style canonical solve goes (dev tool):
 wraps trunc / apply / cp_norm with timers and rank logs, runs batch problem 0
 at the sizes given on the command line."""
+import os
 import sys
 import time
 import collections
@@ -24,6 +25,8 @@ def wrap(mod, name, label, rank_of=None):
         stats[label][1] += dt
         if rank_of is not None:
             log.append((label, rank_of(a, out), round(dt, 4)))
+            if os.environ.get("FL_VERBOSE"):
+                print("   ", log[-1], "mem %.1f GB" % (torch.cuda.max_memory_allocated() / 1e9), flush=True)
         return out
     setattr(mod, name, g)
 
@@ -41,6 +44,9 @@ wrap(decomp, "_merge_collinear", "merge", lambda a, out: (a[0].rank, out.rank))
 wrap(decomp, "cp_norm", "cp_norm(decomp)", lambda a, out: (a[0].rank,))
 wrap(decomp, "_pick_ranks", "pick_ranks")
 wrap(decomp, "rhosvd", "rhosvd")
+for nm in ("_svd", "_left_sv", "_kr_contract", "_cp_project_core", "_range_basis", "_complete_columns", "cp_normalize",
+           "_collinear_pairs", "_kept_rank", "_fix_signs", "_core_cp_als", "_lift_tucker", "_compress_cp"):
+    wrap(decomp, nm, "  ." + nm)
 for n in [int(v) for v in sys.argv[1:]]:
     stats.clear()
     log.clear()
