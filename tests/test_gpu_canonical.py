@@ -252,3 +252,28 @@ def test_svd_batched_matches_numpy(b, m, n):
         Uk, Vk = U[i][:, keep], Vt[i][keep]
         assert np.allclose(Uk.T @ Uk, np.eye(keep.sum()), atol=1e-12)
         assert np.allclose(Vk @ Vk.T, np.eye(keep.sum()), atol=1e-12)
+
+
+def test_apply_compressed_matches_apply_then_trunc(monkeypatch):
+    """trunc(apply_compressed(op, x)) == trunc(apply(op, x)): same kept rank,
+    same tensor far below the truncation tolerance (compression forced on a
+    127^3 grid)."""
+    from paper_1809_01971_b200 import decomp, fracop, spectral
+    n = 127
+    spec = spectral.laplacian_spectrum(n, 3)
+    kind = flop.CoreFunctionKind("g2", 0.5, coeff_minus=1e-2, coeff_plus=1e2)
+    core = fracop.build_core(kind, spec, decomp.TruncationSpec(tolerance=1e-8))
+    op = fracop.LowRankOperator(core)
+    x = _smooth_cp((n, n, n), 40, seed=5)
+    tspec = decomp.TruncationSpec(tolerance=1e-8)
+    want = decomp.trunc(fracop.apply(op, x), tspec)
+    monkeypatch.setattr(decomp, "_COMPRESS_MIN_N", 64)
+    xz = fracop.apply_compressed(op, x)
+    assert isinstance(xz, decomp.CompressedCp) and xz.rank == core.core.rank * x.rank
+    assert all(Q is not None for Q in xz.bases)
+    dense = fracop.apply(op, x)
+    full = xz.materialize()
+    assert fl.cp_norm(fl.cp_add(full, fl.cp_scale(dense, -1.0))) <= 1e-12 * fl.cp_norm(dense)
+    got = decomp.trunc(xz, tspec)
+    assert got.rank == want.rank
+    assert fl.cp_norm(fl.cp_add(got, fl.cp_scale(want, -1.0))) <= 1e-11 * fl.cp_norm(want)
