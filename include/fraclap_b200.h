@@ -148,8 +148,8 @@ int fl_cp_gram(int d, const int64_t* n, const double* const* A, int64_t Ra,
 /* Batched thin SVD of small matrices (one-sided Jacobi, one CTA per
  * matrix): A is batch x m x n row-major; U (batch, m, k), S (batch, k)
  * descending, Vt (batch, k, n), k = min(m, n).  The slice SVDs of t2c
- * (decomp.py:468-519).  Requires (max(m,n)*k + k*k + k) doubles <= 200 KiB
- * (e.g. m = n <= 110). */
+ * (decomp.py:468-519).  Working set in shared memory up to m = n = 110,
+ * beyond that in a device scratch allocated on the stream. */
 int fl_svd_batched(const double* A, int batch, int m, int n, double* U, double* S,
                    double* Vt, void* stream);
 

@@ -40,17 +40,25 @@ __device__ __forceinline__ void rr_pair(int N, int r, int k, int& p, int& q) {
 
 // A: batch of m x n row-major matrices (leading dim n, batch stride m*n).
 // Outputs: U (batch, m, k), S (batch, k), Vt (batch, k, n), k = min(m, n).
+// Placement: W and V in shared memory when both fit, else V (and if need be
+// W) in a global scratch buffer (scratch != nullptr; per matrix M*K + K*K
+// doubles), which stays L2-resident for the sizes of t2c.
 __global__ void __launch_bounds__(SVD_THREADS) k_svd_jacobi(const double* __restrict__ A, int m, int n,
                                                             double* __restrict__ U, double* __restrict__ S,
-                                                            double* __restrict__ Vt, int max_sweeps) {
+                                                            double* __restrict__ Vt, int max_sweeps,
+                                                            double* scratch, int w_in_smem, int v_in_smem) {
   extern __shared__ double sm_svd[];
   const bool tr = m < n;
   const int M = tr ? n : m;  // rows of the working matrix W
   const int K = tr ? m : n;  // columns of W (= number of singular values)
   const int N = K + (K & 1);
-  double* W = sm_svd;              // column-major M x K
-  double* V = sm_svd + (size_t)M * K;  // column-major K x K
-  int* flag = reinterpret_cast<int*>(V + (size_t)K * K);
+  double* gs = scratch ? scratch + (size_t)blockIdx.x * ((size_t)M * K + (size_t)K * K) : nullptr;
+  double* sp = sm_svd;
+  double* W = w_in_smem ? sp : gs;  // column-major M x K
+  if (w_in_smem) sp += (size_t)M * K;
+  double* V = v_in_smem ? sp : gs + (size_t)M * K;  // column-major K x K
+  if (v_in_smem) sp += (size_t)K * K;
+  int* flag = reinterpret_cast<int*>(sp);
   const double* Ab = A + (size_t)blockIdx.x * m * n;
   // load W = A (columns of A) or A^T (rows of A) column-major
   for (int idx = threadIdx.x; idx < m * n; idx += blockDim.x) {
@@ -109,7 +117,7 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd_jacobi(const double* __rest
     if (!any) break;
   }
   // singular values = column norms; rank by decreasing sigma (ties by index)
-  double* sig = reinterpret_cast<double*>(flag + 2);
+  double* sig = reinterpret_cast<double*>(flag + 2);  // K doubles after the flag
   for (int j = warp; j < K; j += nwarps) {
     const double* wj = W + (size_t)j * M;
     double a = 0.0;
@@ -145,23 +153,31 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd_jacobi(const double* __rest
 
 }  // namespace
 
-size_t svd_batched_smem(int m, int n) {
-  const size_t M = m > n ? m : n, K = m < n ? m : n;
-  return sizeof(double) * (M * K + K * K + K) + 2 * sizeof(int);
-}
+constexpr size_t SVD_SMEM_CAP = 200 * 1024;
 
 int svd_batched(const double* A, int batch, int m, int n, double* U, double* S, double* Vt, cudaStream_t st) {
   FL_ARG_CHECK(batch >= 0 && m >= 1 && n >= 1, "bad batched SVD shape (%d, %d, %d)", batch, m, n);
-  const size_t smem = svd_batched_smem(m, n);
-  FL_ARG_CHECK(smem <= 200 * 1024, "batched SVD: %d x %d matrices exceed the shared-memory budget", m, n);
+  const size_t M = m > n ? m : n, K = m < n ? m : n;
+  const size_t wb = sizeof(double) * M * K, vb = sizeof(double) * K * K, tail = sizeof(double) * K + 2 * sizeof(int);
+  FL_ARG_CHECK(tail <= SVD_SMEM_CAP, "batched SVD: %d x %d matrices are too large", m, n);
   if (batch == 0) return FL_OK;
+  int w_sm = 0, v_sm = 0;
+  if (wb + vb + tail <= SVD_SMEM_CAP) {
+    w_sm = v_sm = 1;
+  } else if (wb + tail <= SVD_SMEM_CAP) {
+    w_sm = 1;
+  }
+  const size_t smem = (w_sm ? wb : 0) + (v_sm ? vb : 0) + tail;
+  double* scratch = nullptr;
+  if (!(w_sm && v_sm)) FL_CUDA_TRY(cudaMallocAsync(&scratch, (wb + vb) * (size_t)batch, st));
   static bool attr_set = false;
   if (!attr_set) {
-    FL_CUDA_TRY(cudaFuncSetAttribute(k_svd_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    FL_CUDA_TRY(cudaFuncSetAttribute(k_svd_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SVD_SMEM_CAP));
     attr_set = true;
   }
-  k_svd_jacobi<<<batch, SVD_THREADS, smem, st>>>(A, m, n, U, S, Vt, 40);
+  k_svd_jacobi<<<batch, SVD_THREADS, smem, st>>>(A, m, n, U, S, Vt, 40, scratch, w_sm, v_sm);
   FL_LAUNCH_CHECK();
+  if (scratch) FL_CUDA_TRY(cudaFreeAsync(scratch, st));
   return FL_OK;
 }
 

@@ -225,7 +225,7 @@ def test_trunc_range_compression_matches_uncompressed(dims, R, tol, monkeypatch)
 
 
 @pytest.mark.parametrize("b,m,n", [(5, 7, 7), (64, 64, 64), (3, 40, 17), (4, 17, 40), (2, 96, 96), (1, 1, 5),
-                                   (0, 8, 8)])
+                                   (0, 8, 8), (3, 140, 130), (2, 214, 211), (2, 150, 260)])
 def test_svd_batched_matches_numpy(b, m, n):
     from paper_1809_01971_b200.decomp import svd_batched
     rng = np.random.default_rng(m * n + b)

@@ -38,8 +38,10 @@ if os.environ.get("FL_COMPRESS_MIN_N"):
 _pcg_orig = solver.cp_norm
 wrap(solver, "trunc", "trunc", rin)
 wrap(solver, "apply", "apply", lambda a, out: (a[1].rank, out.rank))
+wrap(solver, "apply_compressed", "apply_compressed", lambda a, out: (a[1].rank, out.rank))
+wrap(decomp, "_range_basis_gen", "  ._range_basis_gen")
 wrap(decomp, "c2t", "c2t")
-wrap(decomp, "t2c", "t2c")
+wrap(decomp, "t2c", "t2c", lambda a, out: (tuple(a[0].core.shape), out.rank))
 wrap(decomp, "_merge_collinear", "merge", lambda a, out: (a[0].rank, out.rank))
 wrap(decomp, "cp_norm", "cp_norm(decomp)", lambda a, out: (a[0].rank,))
 wrap(decomp, "_pick_ranks", "pick_ranks")
@@ -51,7 +53,7 @@ for n in [int(v) for v in sys.argv[1:]]:
     stats.clear()
     log.clear()
     t0 = time.perf_counter()
-    y, cfg = batch.problem(0, n)
+    y, cfg = batch.problem(int(os.environ.get("FL_PROBLEM", "0")), n)
     kind = fracop.CoreFunctionKind("g2", cfg.alpha, coeff_minus=float(cfg.beta), coeff_plus=float(cfg.gamma) / float(cfg.beta))
     spec = __import__("paper_1809_01971_b200").spectral.laplacian_spectrum(n, 3)
     torch.cuda.synchronize(); t1 = time.perf_counter()
