@@ -407,7 +407,39 @@ def run_solves(args, rank, world, dev):
                               "final_residual": res, "dof": n ** 3, "path": path}
     del A, P, y, u
     torch.cuda.empty_cache()
+    if not args.no_batch:
+        out["config4_batch"] = run_batch(args, rank, world, dev)
     return out if rank == 0 else None
+
+
+def run_batch(args, rank, world, dev):
+    """BASELINE configs[4] sample: the first --batch-count problems of the
+    batch distribution at each n of --batch-n, spread over the ranks (no
+    collective on the data path); solves/s from the max-over-ranks time."""
+    import time
+    import torch
+    import torch.distributed as dist
+    from paper_1809_01971_b200 import batch
+
+    per_n = {}
+    for n in [int(v) for v in args.batch_n.split(",") if v]:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        recs = batch.solve_batch(n, args.batch_count, rank, world)
+        torch.cuda.synchronize()
+        t = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([t], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt)
+        per_n[str(n)] = {"problems": args.batch_count, "seconds": t, "solves_per_s": args.batch_count / t,
+                         "rank0_records": [{"alpha": round(r["alpha"], 4), "beta": r["beta"],
+                                            "iterations": r["iterations"], "converged": r["converged"],
+                                            "rank": r["rank"], "seconds": round(r["seconds"], 3)} for r in recs]}
+        torch.cuda.empty_cache()
+    return {"per_n": per_n, "n_gpus": world,
+            "path": "canonical PCG per problem (exp-sum control core, ladder preconditioner <= 1023 "
+                    "interpolated in log eigenvalue, range-compressed truncation), problems spread over ranks"}
 
 
 def main(argv=None):
@@ -420,6 +452,9 @@ def main(argv=None):
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-solves", action="store_true")
     p.add_argument("--solve-n", type=int, default=1023)
+    p.add_argument("--no-batch", action="store_true", help="skip the configs[4] batch sample")
+    p.add_argument("--batch-n", default="1023,2047,4095,8191")
+    p.add_argument("--batch-count", type=int, default=1)
     args = p.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
