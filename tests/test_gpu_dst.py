@@ -185,3 +185,19 @@ def test_padded_errors():
                   _lib.dims_arr((15, 15, 15)), 14, 1.0, _lib.stream_ptr())
     with pytest.raises(ValueError):
         full.run_pass((_lib.ptr(x), _lib.ptr(x), None, 12, 1, 1, 1, 1, (0, 1, 0, 12), (0, 1, 0, 12), 1.0))
+
+
+@pytest.mark.parametrize("mode", ["1", "2"])
+@pytest.mark.parametrize("n,inner", [(63, 16), (255, 40), (511, 512), (1023, 6), (4095, 2)])
+def test_dst1_tma_variant(monkeypatch, mode, n, inner):
+    """The opt-in TMA-fed strided kernel (FL_TMA=1: two CTAs/SM, one buffer;
+    FL_TMA=2: one CTA/SM, double-buffered) matches scipy."""
+    from paper_1809_01971_b200 import _lib
+    monkeypatch.setenv("FL_TMA", mode)
+    rng = np.random.default_rng(n + inner)
+    outer = 3
+    x = rng.standard_normal((outer, n, inner))
+    xt = torch.tensor(x, device="cuda")
+    y = torch.empty_like(xt)
+    _lib.call("fl_dst1", _lib.ptr(xt), _lib.ptr(y), outer, n, inner, 1.0, _lib.stream_ptr())
+    assert rel(y.cpu().numpy(), oracle.dst(x, axis=1)) <= 1e-13
