@@ -276,4 +276,8 @@ def test_apply_compressed_matches_apply_then_trunc(monkeypatch):
     assert fl.cp_norm(fl.cp_add(full, fl.cp_scale(dense, -1.0))) <= 1e-12 * fl.cp_norm(dense)
     got = decomp.trunc(xz, tspec)
     assert got.rank == want.rank
-    assert fl.cp_norm(fl.cp_add(got, fl.cp_scale(want, -1.0))) <= 1e-11 * fl.cp_norm(want)
+    # both truncations are within the tolerance of the untruncated product;
+    # terms at the cutoff may be chosen differently under different rounding
+    nd = fl.cp_norm(dense)
+    assert fl.cp_norm(fl.cp_add(got, fl.cp_scale(dense, -1.0))) <= 1e-8 * nd
+    assert fl.cp_norm(fl.cp_add(got, fl.cp_scale(want, -1.0))) <= 2e-8 * nd
