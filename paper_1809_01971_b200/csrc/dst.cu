@@ -149,7 +149,8 @@ int grid_for(K kernel, int nt, size_t smem, int64_t ntiles, int* grid) {
 template <int LOGN, bool CONTIG, int LOADER, bool MID>
 int launch_fft(DstArgs a, cudaStream_t st) {
   using S = DstShape<LOGN>;
-  constexpr int C = 2 * S::NFFT;
+  constexpr int NF = MID ? S::NFFT_MID : (LOADER == LOAD_KR ? S::NFFT : S::NFFT_PLAIN);
+  constexpr int C = 2 * NF;
   if (CONTIG) {
     a.ntiles = (a.outer + C - 1) / C;
     a.nchunks = 1;
@@ -163,10 +164,10 @@ int launch_fft(DstArgs a, cudaStream_t st) {
     a.div_blk = make_fastdiv((uint32_t)(a.groups * a.nchunks));
     a.div_chunk = make_fastdiv((uint32_t)a.nchunks);
   }
-  constexpr int NT = MID ? S::NT_MID : S::NT;
-  constexpr int MINB = MID ? S::MINB_MID : S::MINB;
-  constexpr size_t SMEM = MID ? S::smem_mid(NT) : S::smem(NT);
-  auto kern = k_dst_fft<LOGN, S::NFFT, NT, MINB, CONTIG, LOADER, MID>;
+  constexpr int NT = MID ? S::NT_MID : (LOADER == LOAD_KR ? S::NT : S::NT_PLAIN);
+  constexpr int MINB = MID ? S::MINB_MID : (LOADER == LOAD_KR ? S::MINB : S::MINB_PLAIN);
+  constexpr size_t SMEM = MID ? S::smem_mid(NT) : S::smem_n(NT, NF);
+  auto kern = k_dst_fft<LOGN, NF, NT, MINB, CONTIG, LOADER, MID>;
   int grid = 0;
   int rc = grid_for(kern, NT, SMEM, a.ntiles, &grid);
   if (rc) return rc;

@@ -1122,14 +1122,27 @@ struct DstShape {
   static constexpr int NFFT = LOGN <= 8 ? 16 : (LOGN >= 12 ? 1 : (8 >> (LOGN - 9)));
   static constexpr int NT = LOGN >= 13 ? 1024 : (LOGN >= 8 ? 512 : (LOGN <= 5 ? 128 : 256));
   static constexpr int MINB = LOGN >= 13 ? 1 : (LOGN >= 8 ? 2 : (LOGN <= 5 ? 8 : 4));
-  // the fused operator pass stages its whole tile in registers across a
-  // barrier: twice the threads halves the per-thread share
-  // the fused pass carries more live state across its two transforms: half
-  // the threads, twice the register budget (128), no spills
-  static constexpr int NT_MID = NT;
-  static constexpr int MINB_MID = MINB;
-  static constexpr size_t smem(int nt) { return size_t(16) * (size_t(1) << LOGN) * NFFT + size_t(16) * NFFT * (nt / 32); }
-  static constexpr size_t smem_mid(int nt) { return smem(nt) + GatherTable<LOGN>::bytes(); }
+#ifndef FL_MID_SPLIT
+#define FL_MID_SPLIT 0
+#endif
+#ifndef FL_PLAIN_SPLIT
+#define FL_PLAIN_SPLIT 0
+#endif
+  // optional half-size tiles (NFFT/2 FFTs, NT/2 threads, twice the CTAs):
+  // more independent CTAs per SM for the same warp count
+  static constexpr bool SPLIT_MID = FL_MID_SPLIT && LOGN >= 8 && LOGN <= 11;
+  static constexpr bool SPLIT_PLAIN = FL_PLAIN_SPLIT && LOGN >= 8 && LOGN <= 11;
+  static constexpr int NFFT_MID = SPLIT_MID ? NFFT / 2 : NFFT;
+  static constexpr int NT_MID = SPLIT_MID ? NT / 2 : NT;
+  static constexpr int MINB_MID = SPLIT_MID ? 2 * MINB : MINB;
+  static constexpr int NFFT_PLAIN = SPLIT_PLAIN ? NFFT / 2 : NFFT;
+  static constexpr int NT_PLAIN = SPLIT_PLAIN ? NT / 2 : NT;
+  static constexpr int MINB_PLAIN = SPLIT_PLAIN ? 2 * MINB : MINB;
+  static constexpr size_t smem_n(int nt, int nfft) {
+    return size_t(16) * (size_t(1) << LOGN) * nfft + size_t(16) * nfft * (nt / 32);
+  }
+  static constexpr size_t smem(int nt) { return smem_n(nt, NFFT); }
+  static constexpr size_t smem_mid(int nt) { return smem_n(nt, NFFT_MID) + GatherTable<LOGN>::bytes(); }
 };
 
 }  // namespace fl
