@@ -11,6 +11,7 @@
 
 #include "dst_fft.cuh"
 #include "dst_tma.cuh"
+#include "dst_reg.cuh"
 #include "kernels.cuh"
 
 namespace fl {
@@ -176,6 +177,45 @@ int launch_fft(DstArgs a, cudaStream_t st) {
   return FL_OK;
 }
 
+// ---- register-resident N = 512 pass (dst_reg.cuh) -------------------------
+bool reg_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FL_REG");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+template <int SIN, int SOUT, bool MID>
+int launch_reg(DstArgs a, cudaStream_t st) {
+  if (SIN == rg::SIDE_CONTIG) {
+    a.ntiles = (a.outer + 15) / 16;
+    a.nchunks = 1;
+  } else {
+    a.nchunks = (a.wv + 15) / 16;
+    a.ntiles = a.outer * a.groups * a.nchunks;
+  }
+  if (a.ntiles == 0) return FL_OK;
+  FL_ARG_CHECK(a.ntiles < (int64_t(1) << 31), "too many DST tiles (%lld)", (long long)a.ntiles);
+  if (SIN != rg::SIDE_CONTIG) {
+    a.div_blk = make_fastdiv((uint32_t)(a.groups * a.nchunks));
+    a.div_chunk = make_fastdiv((uint32_t)a.nchunks);
+  }
+  auto kern = rg::k_dst_grp<SIN, SOUT, MID>;
+  constexpr size_t SMEM = rg::grp_smem_bytes();
+  static bool attr = false;
+  if (!attr) {
+    FL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    attr = true;
+  }
+  const int64_t cap = 2 * (int64_t)sm_count();
+  const int grid = (int)(a.ntiles < cap ? a.ntiles : cap);
+  kern<<<grid, 32 * rg::NWARP, SMEM, st>>>(a);
+  FL_LAUNCH_CHECK();
+  return FL_OK;
+}
+
 // ---- TMA-fed strided pass (dst_tma.cuh) ----------------------------------
 PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -313,6 +353,15 @@ int dst_pass(const double* x, double* y, const double* core, int64_t n, bool con
     auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
     a.vec_in = al(x) && (core == nullptr || al(core)) && in.os % 2 == 0 && in.gp % 2 == 0 && in.js % 2 == 0;
     a.vec_out = al(y) && out.os % 2 == 0 && out.gp % 2 == 0 && out.js % 2 == 0;
+  }
+  if (logn == 9 && reg_enabled()) {
+    if (core == nullptr && !contig) {
+      a.scale = scale * nrm;
+      if (a.vec_in && a.vec_out) return launch_reg<rg::SIDE_VEC, rg::SIDE_VEC, false>(a, st);
+      if (a.vec_in) return launch_reg<rg::SIDE_VEC, rg::SIDE_SCALAR, false>(a, st);
+      if (a.vec_out) return launch_reg<rg::SIDE_SCALAR, rg::SIDE_VEC, false>(a, st);
+      return launch_reg<rg::SIDE_SCALAR, rg::SIDE_SCALAR, false>(a, st);
+    }
   }
   if (core == nullptr) {
     a.scale = scale * nrm;

@@ -1,0 +1,626 @@
+// Register-resident DST-I for N = n + 1 = 512 (the configs[2] grid, n = 511).
+//
+// Same algorithm as dst_fft.cuh (pre-processing y_j = s_j (x_j + x_{N-j}) +
+// (x_j - x_{N-j})/2, two lines per complex FFT, split + segmented scan), but
+// the transform itself lives in registers:
+//   * a warp owns 4 lines (2 packed complex FFTs, 16 lanes each); lane q
+//     holds y_{q + 16 m}, m < 32, and runs the 32-point DFTs in registers;
+//     after the W_512^{q k2} twiddles one warp-private shared-memory exchange
+//     hands lane q the columns k2 = q and q + 16 for the 16-point DFTs
+//     (N = 512 = 32 x 16); a second warp-private staging puts the spectrum in
+//     natural order so that lane q splits k in [16q, 16q + 16) against N - k
+//     and scans its 16 Re Y values in registers (cross-lane offsets by 4
+//     shuffles).  No CTA barrier inside the FFT.
+//   * global traffic is organised per CTA of 4 warps = 16 lines: on strided
+//     layouts every load/store instruction covers whole 128-byte row
+//     segments (a warp's own 4 columns are only 32 bytes of a row; 32-byte
+//     accesses cost 1.8-2.5x the DRAM bytes and stall the LSU).  The CTA's
+//     tile (64 KB, rows of 16 columns, 16-byte chunks XOR-swizzled by row)
+//     is loaded with cp.async; the next tile's loads are issued as soon as
+//     the current one has been read into registers, so they fly during the
+//     FFTs.  Outputs go through the warps' 8 KB scratch in two halves and
+//     leave as full row segments.
+//   * 96 KB of shared memory per CTA, 2 CTAs per SM, up to 255 registers.
+// Every shared-memory and global access is a per-lane base plus a
+// compile-time offset; sines and twiddles come from per-lane constants.
+// Compute-only (no global traffic) the plain pass runs in 0.30 ms at n = 511,
+// the CTA kernel of dst_fft.cuh in 0.47 ms.
+#pragma once
+
+#include <type_traits>
+
+#include "dst_fft.cuh"
+
+namespace fl {
+namespace rg {
+
+constexpr int N = 512, H = 256;
+constexpr int BUF = 1024;  // double2 per warp buffer (16 KB): 512 rows x 2 FFTs
+#ifndef FL_REG_PRE_BATCH
+#define FL_REG_PRE_BATCH 8
+#endif
+constexpr int PRE_BATCH = FL_REG_PRE_BATCH;
+
+// unit sides: 16-byte line pairs on a strided layout, single lines on a
+// strided layout, contiguous lines with an even pitch
+enum { SIDE_VEC = 0, SIDE_SCALAR = 1, SIDE_CONTIG = 2 };
+// shared-memory tile layouts read by the pre-processing
+enum { RAW_STRIDED = 0, RAW_Z = 1, RAW_CONTIG = 2 };
+
+__host__ __device__ constexpr int brev(int v, int bits) {
+  int r = 0;
+  for (int b = 0; b < bits; ++b) r |= ((v >> b) & 1) << (bits - 1 - b);
+  return r;
+}
+
+// cos(pi m / 32), m in [0, 64), from correctly rounded first-quadrant values
+__host__ __device__ constexpr double c64(int m) {
+  constexpr double t[17] = {1.0,
+                            0.9951847266721969,
+                            0.9807852804032304,
+                            0.9569403357322088,
+                            0.9238795325112867,
+                            0.881921264348355,
+                            0.8314696123025452,
+                            0.773010453362737,
+                            0.7071067811865476,
+                            0.6343932841636455,
+                            0.5555702330196022,
+                            0.47139673682599764,
+                            0.3826834323650898,
+                            0.2902846772544624,
+                            0.19509032201612828,
+                            0.0980171403295606,
+                            0.0};
+  m &= 63;
+  return m <= 16 ? t[m] : m <= 32 ? -t[32 - m] : m <= 48 ? -t[m - 32] : t[64 - m];
+}
+// sin(pi m / 32)
+__host__ __device__ constexpr double s64(int m) { return c64(16 - m); }
+
+// The same values in constant memory: with a compile-time index they are
+// constant-bank operands of DFMA/DMUL, whereas FP64 literals are materialised
+// in registers and hoisted out of the unit loop (which spills).
+#define FL_C64_4(b) c64(b), c64(b + 1), c64(b + 2), c64(b + 3)
+#define FL_C64_16(b) FL_C64_4(b), FL_C64_4(b + 4), FL_C64_4(b + 8), FL_C64_4(b + 12)
+__constant__ double kcos64[64] = {FL_C64_16(0), FL_C64_16(16), FL_C64_16(32), FL_C64_16(48)};
+#undef FL_C64_16
+#undef FL_C64_4
+__device__ __forceinline__ double kc(int m) { return kcos64[m & 63]; }
+__device__ __forceinline__ double ks(int m) { return kcos64[(16 - m) & 63]; }
+
+// x * W_32^e, W_32 = exp(-2 pi i / 32); e is a compile-time constant after
+// unrolling, so every branch but one folds away
+__device__ __forceinline__ double2 mulw(double2 x, int e) {
+  constexpr double r = 0.70710678118654752440084436210485;
+  e &= 31;
+  if (e == 0) return x;
+  if (e == 8) return make_double2(x.y, -x.x);
+  if (e == 16) return make_double2(-x.x, -x.y);
+  if (e == 24) return make_double2(-x.y, x.x);
+  if (e == 4) return make_double2((x.x + x.y) * r, (x.y - x.x) * r);
+  if (e == 12) return make_double2((x.y - x.x) * r, -(x.x + x.y) * r);
+  if (e == 20) return make_double2(-(x.x + x.y) * r, (x.x - x.y) * r);
+  if (e == 28) return make_double2((x.x - x.y) * r, (x.x + x.y) * r);
+  const double c = kc(2 * e), s = ks(2 * e);
+  return make_double2(fma(x.x, c, x.y * s), fma(x.y, c, -x.x * s));
+}
+
+// in-register radix-2 DIF FFT, LEN <= 32: v[i] ends up holding X[brev(i)]
+template <int LEN>
+__device__ __forceinline__ void dif(double2 (&v)[LEN]) {
+#pragma unroll
+  for (int half = LEN / 2; half >= 1; half >>= 1) {
+#pragma unroll
+    for (int b = 0; b < LEN; b += 2 * half) {
+#pragma unroll
+      for (int j = 0; j < half; ++j) {
+        const double2 p = v[b + j], c = v[b + j + half];
+        v[b + j] = cadd(p, c);
+        v[b + j + half] = mulw(csub(p, c), j * (32 / (2 * half)));
+      }
+    }
+  }
+}
+
+// ---- shared-memory layouts ------------------------------------------------
+// CTA tile, strided passes: row j (1..511) of the 16 tile columns as 8
+// double2 chunks (columns 2c, 2c+1), chunk c stored at c ^ (j & 7)
+// (the TMA 128-byte swizzle pattern): 8 consecutive rows of one chunk hit 8
+// bank groups.  CTA tile, contiguous passes: [line][512] doubles, row j at j-1.
+constexpr int TILE = 4096;   // double2 (64 KB)
+constexpr int SCR = 512;     // double2 per warp scratch (8 KB)
+constexpr int NWARP = 4;
+
+__host__ __device__ constexpr int tidx(int j, int c) { return j * 8 + (c ^ (j & 7)); }
+// z layout of the fused pass (a warp's 16 KB of the tile): double2 (lines
+// 2f, 2f+1) of row j at 2j + (f ^ bit 2 of j), low three bits XOR bits 5..7 of
+// j: rows q + 16 m (read) and rows 32 apart (written together) are both
+// conflict-free
+__host__ __device__ constexpr int zidx(int j, int f) { return (2 * j + (f ^ ((j >> 2) & 1))) ^ ((j >> 5) & 7); }
+// output staging of strided passes (a warp's scratch, rows r' in [0, 256)):
+// zidx pattern, XOR 2w so that the 8 chunks of one row, read across the 4
+// warps' scratch, land in 8 bank groups
+__host__ __device__ constexpr int sidx(int r, int f, int w) { return zidx(r, f) ^ (2 * w); }
+
+struct Tile {
+  int64_t base;   // element offset of (row 1, column / line 0)
+  int64_t JS, LS;
+  int lmax;       // valid columns / lines of the tile (<= 16)
+};
+
+template <int SIDE, bool OUT>
+__device__ __forceinline__ Tile tile_of(const DstArgs& a, uint32_t t) {
+  Tile r;
+  if (SIDE == SIDE_CONTIG) {
+    const int64_t L0 = (int64_t)t * 16;
+    const int64_t lp = OUT ? a.out_lp : a.in_lp;
+    r.base = L0 * lp;
+    r.JS = 1;
+    r.LS = lp;
+    const int64_t rem = a.outer - L0;
+    r.lmax = (int)(rem < 16 ? rem : 16);
+  } else {
+    const uint32_t o = a.div_blk.div(t);
+    const uint32_t rr = t - o * a.div_blk.d;
+    const uint32_t g = a.div_chunk.div(rr);
+    const int64_t c0 = (int64_t)(rr - g * a.div_chunk.d) * 16;
+    r.base = (int64_t)o * (OUT ? a.out_os : a.in_os) + (int64_t)g * (OUT ? a.out_gp : a.in_gp) + c0;
+    r.JS = OUT ? a.out_js : a.in_js;
+    r.LS = 1;
+    const int64_t rem = a.wv - c0;
+    r.lmax = (int)(rem < 16 ? rem : 16);
+  }
+  return r;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// cp.async with a compile-time shared-memory offset; sz = 0 zero-fills
+template <int OFF>
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src, int sz) {
+  asm volatile("cp.async.cg.shared.global [%0+%3], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(sz), "n"(OFF) : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ void cp8(uint32_t dst, const void* src, int sz) {
+  asm volatile("cp.async.ca.shared.global [%0+%3], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(sz), "n"(OFF) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(K) : "memory");
+}
+
+// compiler-only fence: keeps the scheduler from hoisting a whole phase's
+// loads (64 x 16 B in flight would need every register)
+__device__ __forceinline__ void sched_fence() { asm volatile("" ::: "memory"); }
+
+template <int I, int END, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (I < END) {
+    f(std::integral_constant<int, I>{});
+    static_for<I + 1, END>(f);
+  }
+}
+
+#ifndef FL_REG_NOMEM
+#define FL_REG_NOMEM 0
+#endif
+
+// cp.async loads of strided tile t into the CTA tile (all 4 warps; every
+// instruction covers 4 (16-byte side) or 2 (8-byte side) whole row segments)
+template <int SIDE>
+__device__ __forceinline__ void issue_strided(const DstArgs& a, uint32_t t, uint32_t stile, int w, int lane) {
+  if (FL_REG_NOMEM) return;
+  const Tile tl = tile_of<SIDE, false>(a, t);
+  if constexpr (SIDE == SIDE_VEC) {
+    const int rho = lane >> 3, c = lane & 7;
+    const int j0 = 1 + rho + 4 * w;  // rows j0 + 16 s
+    const uint32_t d = stile + 16u * (uint32_t)tidx(j0, c);
+    const double* src = a.x + tl.base + (int64_t)(j0 - 1) * tl.JS + 2 * c;
+    const int64_t step = 16 * tl.JS;
+    const int sz = 2 * c < tl.lmax ? 16 : 0;
+    static_for<0, 32>([&](auto I) {
+      constexpr int s = decltype(I)::value;
+      if (s < 31 || j0 < 16) cp16<16 * 128 * s>(d, sz ? src : a.x, sz);
+      src += step;
+    });
+  } else {
+    const int rho = lane >> 4, cc = lane & 15;
+    const int j0 = 1 + rho + 2 * w;  // rows j0 + 8 s
+    const uint32_t d = stile + 8u * (uint32_t)(2 * tidx(j0, cc >> 1) + (cc & 1));
+    const double* src = a.x + tl.base + (int64_t)(j0 - 1) * tl.JS + cc;
+    const int64_t step = 8 * tl.JS;
+    const int sz = cc < tl.lmax ? 8 : 0;
+    static_for<0, 64>([&](auto I) {
+      constexpr int s = decltype(I)::value;
+      if (s < 63 || j0 < 8) cp8<8 * 128 * s>(d, sz ? src : a.x, sz);
+      src += step;
+    });
+  }
+}
+
+// cp.async loads of warp w's 4 lines of contiguous tile t ([line][512])
+__device__ __forceinline__ void issue_contig(const DstArgs& a, uint32_t t, uint32_t stile, int w, int lane) {
+  if (FL_REG_NOMEM) return;
+  const Tile tl = tile_of<SIDE_CONTIG, false>(a, t);
+  const uint32_t d = stile + 8u * (uint32_t)(4 * w * 512) + 16u * (uint32_t)lane;
+  static_for<0, 4>([&](auto L) {
+    constexpr int l = decltype(L)::value;
+    const int sz = 4 * w + l < tl.lmax ? 16 : 0;
+    const double* src = a.x + tl.base + (int64_t)(4 * w + l) * tl.LS + 2 * lane;
+    static_for<0, 8>([&](auto I) {
+      constexpr int i = decltype(I)::value;
+      cp16<8 * (l * 512 + 64 * i)>(d, sz ? src + 64 * i : a.x, sz);
+    });
+  });
+}
+
+struct Lane {
+  int f, q;
+  double sq, cq;             // sin, cos of pi q / 512
+  double2 w1, w8, w16, w24;  // W_512^{q}, ^{8q}, ^{16q}, ^{24q}
+};
+
+__device__ __forceinline__ double launder_d(double v) {
+  double r;
+  asm volatile("mov.b64 %0, %1;" : "=d"(r) : "d"(v));
+  return r;
+}
+__device__ __forceinline__ double2 launder_d2(double2 v) { return make_double2(launder_d(v.x), launder_d(v.y)); }
+
+// Per-tile copy of the lane constants through opaque moves: everything the
+// tile derives from them (32 sines, 31 twiddles) is loop-invariant, and the
+// compiler would otherwise hoist it all out of the tile loop and spill it.
+__device__ __forceinline__ Lane fresh(const Lane& c) {
+  Lane r;
+  r.f = c.f;
+  r.q = c.q;
+  r.sq = launder_d(c.sq);
+  r.cq = launder_d(c.cq);
+  r.w1 = launder_d2(c.w1);
+  r.w8 = launder_d2(c.w8);
+  r.w16 = launder_d2(c.w16);
+  r.w24 = launder_d2(c.w24);
+  return r;
+}
+
+__device__ __forceinline__ Lane lane_consts(const DstArgs& a, int lane) {
+  Lane c;
+  c.f = lane >> 4;
+  c.q = lane & 15;
+  c.sq = __ldg(&a.sn[c.q]);
+  c.cq = __ldg(&a.sn[H - c.q]);
+  c.w1 = __ldg(&a.tw[c.q]);
+  c.w8 = __ldg(&a.tw[(8 * c.q) & (N - 1)]);
+  c.w16 = __ldg(&a.tw[(16 * c.q) & (N - 1)]);
+  c.w24 = __ldg(&a.tw[(24 * c.q) & (N - 1)]);
+  return c;
+}
+
+// DST-I pre-processing of rows j and N - j into y_j (m = row block, j = q + 16 m)
+__device__ __forceinline__ double2 pre_y(const Lane& c, int m, double2 xa, double2 xb) {
+  const double s = fma(c.sq, kc(m), c.cq * ks(m));  // sin(pi (q + 16 m) / 512)
+  const double sp = s + 0.5, sm = s - 0.5;
+  double2 y = make_double2(fma(sp, xa.x, sm * xb.x), fma(sp, xa.y, sm * xb.y));
+  if (m == 0 && c.q == 0) y = make_double2(0.0, 0.0);
+  if (m == 16 && c.q == 0) y = make_double2(2.0 * xa.x, 2.0 * xa.y);
+  return y;
+}
+
+// pre-processed input y_{q + 16 m} of FFT f of warp w
+template <int RAW>
+__device__ __forceinline__ void pre_read(const double2* tile, int w, const Lane& c, double2 (&v)[32]) {
+  const int f = c.f, q = c.q, q7 = q & 7;
+  if constexpr (RAW == RAW_CONTIG) {
+    const double* d = reinterpret_cast<const double*>(tile) + (4 * w + 2 * f) * 512;
+    const double* pa = d + q - 1;    // row j at j - 1
+    const double* pb = d + 511 - q;  // row N - j, j = q + 16 m
+#pragma unroll
+    for (int m = 0; m < 32; ++m) {
+      if (m % PRE_BATCH == 0) sched_fence();
+      const double* qa = (m == 0) ? (q == 0 ? pb : pa) : pa + 16 * m;
+      const double* qb = pb - 16 * m;
+      v[m] = pre_y(c, m, make_double2(qa[0], qa[512]), make_double2(qb[0], qb[512]));
+    }
+  } else if constexpr (RAW == RAW_STRIDED) {
+    const int ch = 2 * w + f;
+    const int la = tidx(q, ch);                                               // + 128 m
+    const int lb = q == 0 ? 128 + ch : (16 - q) * 8 + (ch ^ ((8 - q7) & 7));  // + 128 (31 - m)
+#pragma unroll
+    for (int m = 0; m < 32; ++m) {
+      if (m % PRE_BATCH == 0) sched_fence();
+      const int ia = la + 128 * m;
+      const int ib = (m == 0 && q == 0) ? la : lb + 128 * (31 - m);
+      v[m] = pre_y(c, m, tile[ia], tile[ib]);
+    }
+  } else {
+    // z layout in warp w's 16 KB of the tile
+    const double2* zt = tile + 1024 * w;
+    const int la = zidx(q, f);
+    const int lb = q == 0 ? 32 + f : zidx(16 - q, f);
+#pragma unroll
+    for (int m = 0; m < 32; ++m) {
+      if (m % PRE_BATCH == 0) sched_fence();
+      // bits 5..7 of the row: (m >> 1) for row q + 16 m, (31 - m) >> 1 for the
+      // partner row (16 - q) + 16 (31 - m), (32 - m) >> 1 for q = 0 (row 16 (32 - m))
+      const int ia = (la ^ ((m >> 1) & 7)) + 32 * m;
+      int ib = q == 0 ? ((lb ^ (((32 - m) >> 1) & 7)) + 32 * (31 - m)) : ((lb ^ (((31 - m) >> 1) & 7)) + 32 * (31 - m));
+      if (m == 0 && q == 0) ib = ia;
+      v[m] = pre_y(c, m, zt[ia], zt[ib]);
+    }
+  }
+}
+
+// FFT of the pre-processed v (lane q of FFT f), split, scan, with the warp's
+// 8 KB scratch.  On return ev[i] = S'_{2k}, od[i] = S'_{2k+1} for
+// k = 16 q + i, S' = 2 * DST_raw (lines 2f / 2f+1 in .x / .y; ev[0] of lane
+// 0 is S_0, unused).
+__device__ __forceinline__ void fft_split(double2* scr, const Lane& c, double2 (&v)[32], double2 (&ev)[16],
+                                          double2 (&od)[16]) {
+  const int f = c.f, q = c.q, q7 = q & 7;
+  double2* sf = scr + f * 256;
+  dif<32>(v);
+  // exchange in two rounds (k2 < 16, k2 >= 16): [k2'][q' ^ (k2' & 7)]
+  // twiddles W_512^{q k2}, k2 = 8 h + l: W^{8qh} exact, then products by W^q
+  double2 w0[16], w1[16];
+#pragma unroll
+  for (int rd = 0; rd < 2; ++rd) {
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int h = 2 * rd + hh;
+      double2 t = h == 1 ? c.w8 : h == 2 ? c.w16 : c.w24;
+#pragma unroll
+      for (int l = 0; l < 8; ++l) {
+        const int k2 = 8 * h + l;
+        double2 val = v[brev(k2, 5)];
+        if (h == 0 && l == 1) t = c.w1;
+        if ((h == 0 && l >= 2) || (h > 0 && l >= 1)) t = cmul(t, c.w1);
+        if (k2) val = cmul(val, t);
+        const int kk = k2 & 15;
+        sf[kk * 16 + (q ^ (kk & 7))] = val;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int qq = 0; qq < 16; ++qq) {
+      const double2 x = sf[q * 16 + (qq ^ q7)];
+      if (rd == 0) w0[qq] = x; else w1[qq] = x;
+    }
+    __syncwarp();
+  }
+  dif<16>(w0);
+  dif<16>(w1);
+  // spectrum staging in two rounds: k < 256 (k1 < 8), then k >= 256; entry
+  // kk = k mod 256 at kk ^ ((kk >> 4) & 7)
+  double2 ck[16], cm[16];
+#pragma unroll
+  for (int rd = 0; rd < 2; ++rd) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int k1 = brev(i, 4);
+      if ((k1 >> 3) != rd) continue;
+      const int k1l = k1 & 7;
+      sf[32 * k1l + (q ^ ((2 * k1l) & 7))] = w0[i];
+      sf[32 * k1l + 16 + (q ^ ((2 * k1l + 1) & 7))] = w1[i];
+    }
+    __syncwarp();
+    if (rd == 0) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) ck[i] = sf[16 * q + (i ^ q7)];
+    } else {
+      // partner N - k of k = 16q + i: kk = 16 (15 - q) + (16 - i) for i >= 1,
+      // 16 (16 - q) for i = 0 (q >= 1); k = 0 pairs with itself
+#pragma unroll
+      for (int i = 1; i < 16; ++i) cm[i] = sf[16 * (15 - q) + ((16 - i) ^ ((7 - q7) & 7))];
+      cm[0] = q == 0 ? ck[0] : sf[16 * (16 - q) + ((16 - q) & 7)];
+    }
+    __syncwarp();
+  }
+  double2 run = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    double2 r = make_double2(ck[i].x + cm[i].x, ck[i].y + cm[i].y);
+    ev[i] = make_double2(cm[i].y - ck[i].y, ck[i].x - cm[i].x);
+    if (i == 0 && q == 0) r = ck[0];  // R_0 / 2 seeds S_1
+    run.x += r.x;
+    run.y += r.y;
+    od[i] = run;
+  }
+  // exclusive offsets over the 16 lanes of this FFT
+  double2 inc = run;
+#pragma unroll
+  for (int d = 1; d < 16; d <<= 1) {
+    const double ux = __shfl_up_sync(0xffffffffu, inc.x, d, 16);
+    const double uy = __shfl_up_sync(0xffffffffu, inc.y, d, 16);
+    if (q >= d) {
+      inc.x += ux;
+      inc.y += uy;
+    }
+  }
+  const double2 off = make_double2(inc.x - run.x, inc.y - run.y);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    od[i].x += off.x;
+    od[i].y += off.y;
+  }
+}
+
+// strided output, half hh (rows [256 hh, 256 hh + 256)): stage the lane's rows
+// in its warp's scratch, then the CTA writes whole row segments
+template <int SIDE_OUT>
+__device__ __forceinline__ void store_strided(const DstArgs& a, uint32_t t, double2* scr_all, int w, int lane,
+                                              const Lane& c, const double2 (&ev)[16], const double2 (&od)[16],
+                                              double sc) {
+  const int f = c.f, q = c.q;
+  const Tile tl = tile_of<SIDE_OUT, true>(a, t);
+  double2* sw = scr_all + SCR * w;
+#pragma unroll 1
+  for (int hh = 0; hh < 2; ++hh) {
+    // lane q holds rows [32 q, 32 q + 32): half hh is lanes q in [8 hh, 8 hh + 8)
+    if ((q >> 3) == hh) {
+      const int q7 = q & 7;
+      double2* b = sw + 64 * q7;  // rows r' = 32 q7 + ..: sidx = 64 q7 + (zidx(r' & 31) ^ q7 ^ 2w)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const double2 e = make_double2(sc * ev[i].x, sc * ev[i].y);
+        const double2 o = make_double2(sc * od[i].x, sc * od[i].y);
+        if (i > 0 || q > 0) b[zidx(2 * i, f) ^ q7 ^ (2 * w)] = e;
+        b[zidx(2 * i + 1, f) ^ q7 ^ (2 * w)] = o;
+      }
+    }
+    __syncthreads();
+    if (!FL_REG_NOMEM || a.scale == 12345.0) {
+      if constexpr (SIDE_OUT == SIDE_VEC) {
+        const int rho = lane >> 3, ch = lane & 7;
+        const double2* src = scr_all + SCR * (ch >> 1);
+        const bool ok = 2 * ch < tl.lmax;
+        double* y = a.y + tl.base + 2 * ch;
+#pragma unroll 4
+        for (int s = 0; s < 16; ++s) {
+          const int rp = 4 * w + rho + 16 * s;  // r' in [0, 256)
+          const int r = rp + 256 * hh;
+          const double2 val = src[sidx(rp, ch & 1, ch >> 1)];
+          if (ok && r >= 1 && r < N) *reinterpret_cast<double2*>(y + (int64_t)(r - 1) * tl.JS) = val;
+        }
+      } else {
+        const int rho = lane >> 4, cc = lane & 15, ch = cc >> 1;
+        const double* src = reinterpret_cast<const double*>(scr_all + SCR * (ch >> 1));
+        const bool ok = cc < tl.lmax;
+        double* y = a.y + tl.base + cc;
+#pragma unroll 4
+        for (int s = 0; s < 32; ++s) {
+          const int rp = 2 * w + rho + 8 * s;
+          const int r = rp + 256 * hh;
+          const double val = src[2 * sidx(rp, ch & 1, ch >> 1) + (cc & 1)];
+          if (ok && r >= 1 && r < N) y[(int64_t)(r - 1) * tl.JS] = val;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// contiguous output of warp w (lines 4w .. 4w+3 of the tile), half hh: rows
+// r in [256 hh, 256 hh + 256) at staging position p = r - 256 hh of line l,
+// word l * 256 + (p ^ (((p >> 5) & 7) << 1 | (l >> 1))), then 256-byte
+// coalesced stores per instruction
+__device__ __forceinline__ void store_contig(const DstArgs& a, uint32_t t, double2* scr, int w, int lane,
+                                             const Lane& c, const double2 (&ev)[16], const double2 (&od)[16],
+                                             double sc) {
+  const int f = c.f, q = c.q;
+  const Tile tl = tile_of<SIDE_CONTIG, true>(a, t);
+  double* sd = reinterpret_cast<double*>(scr);
+#pragma unroll 1
+  for (int hh = 0; hh < 2; ++hh) {
+    if ((q >> 3) == hh) {
+      const int q7 = q & 7;
+      // rows 32 q + 2 i (+1): p = 32 q7 + 2 i (+1); key = q7 << 1 | f (line 2f or 2f+1 has l >> 1 = f)
+      double* b0 = sd + (2 * f) * 256 + 32 * q7;
+      double* b1 = b0 + 256;
+      const int key = (q7 << 1) | f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int pe = (2 * i) ^ key, po = (2 * i + 1) ^ key;
+        if (i > 0 || q > 0) {
+          b0[pe] = sc * ev[i].x;
+          b1[pe] = sc * ev[i].y;
+        }
+        b0[po] = sc * od[i].x;
+        b1[po] = sc * od[i].y;
+      }
+    }
+    __syncwarp();
+    if (!FL_REG_NOMEM || a.scale == 12345.0) {
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        if (4 * w + l < tl.lmax) {
+          double* y = a.y + tl.base + (int64_t)(4 * w + l) * tl.LS + 256 * hh - 1;  // row r at r - 1
+#pragma unroll
+          for (int s = 0; s < 8; ++s) {
+            const int p = lane + 32 * s;
+            const int r = p + 256 * hh;
+            const double val = sd[l * 256 + (p ^ ((((p >> 5) & 7) << 1) | (l >> 1)))];
+            if (r >= 1 && r < N) y[p] = val;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Persistent CTAs of 4 warps (one 16-line tile at a time), 2 per SM.
+// Strided passes (SIDE_IN != SIDE_CONTIG): CTA-cooperative loads and stores.
+// Contiguous fused pass (MID): warp-local loads, core from the lane-ordered
+// core layout (fl_core_lanes), z through the warp's part of the tile.
+template <int SIDE_IN, int SIDE_OUT, bool MID>
+__global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a) {
+  extern __shared__ __align__(1024) double2 smem_grp[];
+  double2* const tile = smem_grp;
+  double2* const scr_all = smem_grp + TILE;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* const scr = scr_all + SCR * w;
+  const uint32_t stile = smem_u32(tile);
+  const Lane c0 = lane_consts(a, lane);
+  const uint32_t ntiles = (uint32_t)a.ntiles;
+  uint32_t t = blockIdx.x;
+  constexpr bool STRIDED = SIDE_IN != SIDE_CONTIG;
+  if (t < ntiles) {
+    if (STRIDED) issue_strided<SIDE_IN>(a, t, stile, w, lane); else issue_contig(a, t, stile, w, lane);
+  }
+  cp_commit();
+  for (; t < ntiles; t += gridDim.x) {
+    const uint32_t tn = t + gridDim.x;
+    cp_wait<0>();
+    if (STRIDED) __syncthreads(); else __syncwarp();
+    const Lane c = fresh(c0);
+    double2 v[32], ev[16], od[16];
+    pre_read<STRIDED ? RAW_STRIDED : RAW_CONTIG>(tile, w, c, v);
+    if constexpr (!MID) {
+      if (STRIDED) __syncthreads(); else __syncwarp();
+      if (tn < ntiles) {
+        if (STRIDED) issue_strided<SIDE_IN>(a, tn, stile, w, lane); else issue_contig(a, tn, stile, w, lane);
+      }
+      cp_commit();
+      fft_split(scr, c, v, ev, od);
+    } else {
+      __syncwarp();
+      fft_split(scr, c, v, ev, od);
+      // z = S' .* core, rows 2k, 2k+1 (k = 16 q + i), into the warp's part of
+      // the tile; the core comes lane-ordered: entry (unit, row offset i', lane)
+      sched_fence();
+      {
+        const double2* cl = reinterpret_cast<const double2*>(a.core) + ((size_t)(4 * t + w) * 32) * 32 + lane;
+        double2* zt = tile + 1024 * w + 64 * c.q;
+        const int q7 = c.q & 7;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if (i % 4 == 0) sched_fence();
+          const double2 ce = __ldg(cl + 32 * (2 * i)), co = __ldg(cl + 32 * (2 * i + 1));
+          if (i > 0 || c.q > 0) zt[zidx(2 * i, c.f) ^ q7] = make_double2(ev[i].x * ce.x, ev[i].y * ce.y);
+          zt[zidx(2 * i + 1, c.f) ^ q7] = make_double2(od[i].x * co.x, od[i].y * co.y);
+        }
+      }
+      __syncwarp();
+      const Lane c2 = fresh(c0);
+      pre_read<RAW_Z>(tile, w, c2, v);
+      __syncwarp();
+      if (tn < ntiles) issue_contig(a, tn, stile, w, lane);
+      cp_commit();
+      fft_split(scr, c2, v, ev, od);
+    }
+    const double sc = (MID ? 0.25 : 0.5) * a.scale;
+    if constexpr (STRIDED) {
+      store_strided<SIDE_OUT>(a, t, scr_all, w, lane, c0, ev, od, sc);
+    } else {
+      store_contig(a, t, scr, w, lane, c0, ev, od, sc);
+    }
+  }
+  cp_wait<0>();
+}
+
+constexpr size_t grp_smem_bytes() { return (size_t)(TILE + NWARP * SCR) * sizeof(double2); }
+
+}  // namespace rg
+}  // namespace fl
