@@ -115,6 +115,24 @@ int fl_apply_full_padded(const double* x, double* y, const double* core_p, doubl
                          int d, const int64_t* dims, int64_t pitch, double alpha,
                          void* stream);
 
+/* Same operator for n_last = 511 (N = 512, the configs[2] grid) with the
+ * core in lane order, the layout the register-resident fused pass reads
+ * with one coalesced 512-byte load per warp instruction: for 4-line unit u
+ * (lines 4u .. 4u+3 of the padded [line][pitch = 512] view, line = index
+ * over all but the last mode), row offset i in [0, 32) and lane
+ * l = 16 f + q, entry ((u * 32 + i) * 32 + l) is the double pair
+ * (G[line 4u + 2f][row 32q + i], G[line 4u + 2f + 1][row 32q + i]), rows
+ * 1-based (row 0 is zero); units are padded to a multiple of 4 (16 lines).
+ * work as for fl_apply_full_padded (pitch 512).  d = 2 or 3. */
+int fl_apply_full_lanes(const double* x, double* y, const double* core_l, double* work,
+                        int d, const int64_t* dims, double alpha, void* stream);
+
+/* The fused last-mode pass of fl_apply_full_lanes on its own (per-pass
+ * timing): `lines` contiguous lines of pitch `pitch` (>= 512, even),
+ * y = scale * F diag(core_l) F x per line, n = 511.  x == y allowed. */
+int fl_dst1_core_lanes(const double* x, double* y, const double* core_l, int64_t lines,
+                       int64_t pitch, double scale, void* stream);
+
 /* One DST-I pass with explicit layouts (the building block of the two
  * calls above; exposed for per-pass timing).  contig != 0: `outer` lines,
  * row j of line L at L*lp + j.  contig == 0: `outer` blocks of `groups`

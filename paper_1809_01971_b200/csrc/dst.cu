@@ -182,7 +182,7 @@ bool reg_enabled() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("FL_REG");
-    v = (e && e[0] == '1') ? 1 : 0;
+    v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
 }
@@ -385,6 +385,33 @@ int dst_pass(const double* x, double* y, const double* core, int64_t n, bool con
 }
 
 bool fft_length(int64_t n) { return fft_len_ok(n); }
+
+int dst_pass_lanes(const double* x, double* y, const double* core_l, int64_t lines, int64_t pitch, double scale,
+                   cudaStream_t st) {
+  FL_ARG_CHECK(x != nullptr && y != nullptr && core_l != nullptr, "null pointer");
+  FL_ARG_CHECK(lines >= 0 && pitch >= 512 && pitch % 2 == 0 && pitch < (1ll << 31),
+               "lane-core pass: pitch must be even and >= 512, got %lld", (long long)pitch);
+  auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  FL_ARG_CHECK(al(x) && al(y) && al(core_l), "lane-core pass: 16-byte aligned buffers required");
+  if (lines == 0) return FL_OK;
+  const Tables* t = nullptr;
+  int rc = get_tables(511, &t);
+  if (rc) return rc;
+  const double nrm = std::sqrt(2.0 / 512.0);
+  DstArgs a{};
+  a.x = x;
+  a.y = y;
+  a.outer = lines;
+  a.n = 511;
+  a.groups = 1;
+  a.wv = 1;
+  a.in_lp = a.out_lp = pitch;
+  a.core = core_l;
+  a.tw = t->tw;
+  a.sn = t->sn;
+  a.scale = scale * nrm * nrm;
+  return launch_reg<rg::SIDE_CONTIG, rg::SIDE_CONTIG, true>(a, st);
+}
 
 // y = scale * F_n x along the middle axis (optionally core-scaled sandwich)
 int dst_mode(const double* x, double* y, int64_t outer, int64_t n, int64_t inner, double scale,

@@ -217,24 +217,25 @@ __device__ __forceinline__ void issue_strided(const DstArgs& a, uint32_t t, uint
     const int rho = lane >> 3, c = lane & 7;
     const int j0 = 1 + rho + 4 * w;  // rows j0 + 16 s
     const uint32_t d = stile + 16u * (uint32_t)tidx(j0, c);
-    const double* src = a.x + tl.base + (int64_t)(j0 - 1) * tl.JS + 2 * c;
-    const int64_t step = 16 * tl.JS;
     const int sz = 2 * c < tl.lmax ? 16 : 0;
+    // zero-filled chunks read nothing; their source stays at a.x
+    const double* src = sz ? a.x + tl.base + (int64_t)(j0 - 1) * tl.JS + 2 * c : a.x;
+    const int64_t step = sz ? 16 * tl.JS : 0;
     static_for<0, 32>([&](auto I) {
       constexpr int s = decltype(I)::value;
-      if (s < 31 || j0 < 16) cp16<16 * 128 * s>(d, sz ? src : a.x, sz);
+      if (s < 31 || j0 < 16) cp16<16 * 128 * s>(d, src, sz);
       src += step;
     });
   } else {
     const int rho = lane >> 4, cc = lane & 15;
     const int j0 = 1 + rho + 2 * w;  // rows j0 + 8 s
     const uint32_t d = stile + 8u * (uint32_t)(2 * tidx(j0, cc >> 1) + (cc & 1));
-    const double* src = a.x + tl.base + (int64_t)(j0 - 1) * tl.JS + cc;
-    const int64_t step = 8 * tl.JS;
     const int sz = cc < tl.lmax ? 8 : 0;
+    const double* src = sz ? a.x + tl.base + (int64_t)(j0 - 1) * tl.JS + cc : a.x;
+    const int64_t step = sz ? 8 * tl.JS : 0;
     static_for<0, 64>([&](auto I) {
       constexpr int s = decltype(I)::value;
-      if (s < 63 || j0 < 8) cp8<8 * 128 * s>(d, sz ? src : a.x, sz);
+      if (s < 63 || j0 < 8) cp8<8 * 128 * s>(d, src, sz);
       src += step;
     });
   }
@@ -262,39 +263,52 @@ struct Lane {
   double2 w1, w8, w16, w24;  // W_512^{q}, ^{8q}, ^{16q}, ^{24q}
 };
 
+// opaque read-only loads: the lane constants are re-read (L1 hits) for every
+// tile instead of living in registers across the tile loop; everything
+// derived from them (32 sines, 31 twiddles) is loop-invariant, and a plain
+// load would let the compiler hoist it all out of the loop and spill it
 __device__ __forceinline__ double launder_d(double v) {
   double r;
   asm volatile("mov.b64 %0, %1;" : "=d"(r) : "d"(v));
   return r;
 }
-__device__ __forceinline__ double2 launder_d2(double2 v) { return make_double2(launder_d(v.x), launder_d(v.y)); }
 
-// Per-tile copy of the lane constants through opaque moves: everything the
-// tile derives from them (32 sines, 31 twiddles) is loop-invariant, and the
-// compiler would otherwise hoist it all out of the tile loop and spill it.
-__device__ __forceinline__ Lane fresh(const Lane& c) {
-  Lane r;
-  r.f = c.f;
-  r.q = c.q;
-  r.sq = launder_d(c.sq);
-  r.cq = launder_d(c.cq);
-  r.w1 = launder_d2(c.w1);
-  r.w8 = launder_d2(c.w8);
-  r.w16 = launder_d2(c.w16);
-  r.w24 = launder_d2(c.w24);
+__device__ __forceinline__ double ld_opaque(const double* p) {
+  double r;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double2 ld_opaque2(const double2* p) {
+  double2 r;
+  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
   return r;
 }
 
-__device__ __forceinline__ Lane lane_consts(const DstArgs& a, int lane) {
+__device__ __forceinline__ int launder_i(int v) {
+  int r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+template <class T>
+__device__ __forceinline__ T* launder_p(T* p) {
+  T* r;
+  asm volatile("mov.b64 %0, %1;" : "=l"(r) : "l"(p));
+  return r;
+}
+
+// lane constants, re-derived per tile (lane index laundered: the smem
+// offsets computed from q are loop-invariant too)
+__device__ __forceinline__ Lane lane_consts(const DstArgs& a, int lane_in) {
   Lane c;
+  const int lane = launder_i(lane_in);
   c.f = lane >> 4;
   c.q = lane & 15;
-  c.sq = __ldg(&a.sn[c.q]);
-  c.cq = __ldg(&a.sn[H - c.q]);
-  c.w1 = __ldg(&a.tw[c.q]);
-  c.w8 = __ldg(&a.tw[(8 * c.q) & (N - 1)]);
-  c.w16 = __ldg(&a.tw[(16 * c.q) & (N - 1)]);
-  c.w24 = __ldg(&a.tw[(24 * c.q) & (N - 1)]);
+  c.sq = ld_opaque(a.sn + c.q);
+  c.cq = ld_opaque(a.sn + H - c.q);
+  c.w1 = ld_opaque2(a.tw + c.q);
+  c.w8 = ld_opaque2(a.tw + ((8 * c.q) & (N - 1)));
+  c.w16 = ld_opaque2(a.tw + ((16 * c.q) & (N - 1)));
+  c.w24 = ld_opaque2(a.tw + ((24 * c.q) & (N - 1)));
   return c;
 }
 
@@ -310,15 +324,25 @@ __device__ __forceinline__ double2 pre_y(const Lane& c, int m, double2 xa, doubl
 
 // pre-processed input y_{q + 16 m} of FFT f of warp w
 template <int RAW>
-__device__ __forceinline__ void pre_read(const double2* tile, int w, const Lane& c, double2 (&v)[32]) {
+__device__ __forceinline__ void pre_read(const double2* tile, int w, const Lane& c_in, double2 (&v)[32]) {
+  Lane c = c_in;
   const int f = c.f, q = c.q, q7 = q & 7;
+  // each batch's sines are computed from freshly laundered sin/cos, so the
+  // compiler cannot precompute all 32 of them ahead of the loads
+  auto batch = [&](int m) {
+    if (m % PRE_BATCH == 0) {
+      sched_fence();
+      c.sq = launder_d(c.sq);
+      c.cq = launder_d(c.cq);
+    }
+  };
   if constexpr (RAW == RAW_CONTIG) {
     const double* d = reinterpret_cast<const double*>(tile) + (4 * w + 2 * f) * 512;
     const double* pa = d + q - 1;    // row j at j - 1
     const double* pb = d + 511 - q;  // row N - j, j = q + 16 m
 #pragma unroll
     for (int m = 0; m < 32; ++m) {
-      if (m % PRE_BATCH == 0) sched_fence();
+      batch(m);
       const double* qa = (m == 0) ? (q == 0 ? pb : pa) : pa + 16 * m;
       const double* qb = pb - 16 * m;
       v[m] = pre_y(c, m, make_double2(qa[0], qa[512]), make_double2(qb[0], qb[512]));
@@ -329,7 +353,7 @@ __device__ __forceinline__ void pre_read(const double2* tile, int w, const Lane&
     const int lb = q == 0 ? 128 + ch : (16 - q) * 8 + (ch ^ ((8 - q7) & 7));  // + 128 (31 - m)
 #pragma unroll
     for (int m = 0; m < 32; ++m) {
-      if (m % PRE_BATCH == 0) sched_fence();
+      batch(m);
       const int ia = la + 128 * m;
       const int ib = (m == 0 && q == 0) ? la : lb + 128 * (31 - m);
       v[m] = pre_y(c, m, tile[ia], tile[ib]);
@@ -341,7 +365,7 @@ __device__ __forceinline__ void pre_read(const double2* tile, int w, const Lane&
     const int lb = q == 0 ? 32 + f : zidx(16 - q, f);
 #pragma unroll
     for (int m = 0; m < 32; ++m) {
-      if (m % PRE_BATCH == 0) sched_fence();
+      batch(m);
       // bits 5..7 of the row: (m >> 1) for row q + 16 m, (31 - m) >> 1 for the
       // partner row (16 - q) + 16 (31 - m), (32 - m) >> 1 for q = 0 (row 16 (32 - m))
       const int ia = (la ^ ((m >> 1) & 7)) + 32 * m;
@@ -447,12 +471,12 @@ __device__ __forceinline__ void fft_split(double2* scr, const Lane& c, double2 (
 }
 
 // strided output, half hh (rows [256 hh, 256 hh + 256)): stage the lane's rows
-// in its warp's scratch, then the CTA writes whole row segments
+// in its warp's scratch, then the CTA writes whole row segments.  Row
+// r' = r0 + 16 s of the half (r0 = 4w + rho lane-constant) sits at
+// sidx(r', f', w') = 32 s + (b ^ ((s >> 1) & 7)) with b lane-constant.
 template <int SIDE_OUT>
-__device__ __forceinline__ void store_strided(const DstArgs& a, uint32_t t, double2* scr_all, int w, int lane,
-                                              const Lane& c, const double2 (&ev)[16], const double2 (&od)[16],
-                                              double sc) {
-  const int f = c.f, q = c.q;
+__device__ __forceinline__ void store_strided(const DstArgs& a, uint32_t t, double2* scr_all, int w, int lane, int f,
+                                              int q, const double2 (&ev)[16], const double2 (&od)[16], double sc) {
   const Tile tl = tile_of<SIDE_OUT, true>(a, t);
   double2* sw = scr_all + SCR * w;
 #pragma unroll 1
@@ -472,29 +496,37 @@ __device__ __forceinline__ void store_strided(const DstArgs& a, uint32_t t, doub
     __syncthreads();
     if (!FL_REG_NOMEM || a.scale == 12345.0) {
       if constexpr (SIDE_OUT == SIDE_VEC) {
-        const int rho = lane >> 3, ch = lane & 7;
-        const double2* src = scr_all + SCR * (ch >> 1);
+        const int rho = lane >> 3, ch = lane & 7, fo = ch & 1, wo = ch >> 1;
+        const int r0 = 4 * w + rho;  // rows r' = r0 + 16 s
+        const double2* src = scr_all + SCR * wo;
+        const int b = (2 * r0 + (fo ^ ((r0 >> 2) & 1))) ^ (2 * wo);
         const bool ok = 2 * ch < tl.lmax;
-        double* y = a.y + tl.base + 2 * ch;
-#pragma unroll 4
+        const int64_t JS16 = 16 * tl.JS;
+        double* y = a.y + tl.base + 2 * ch + (int64_t)(r0 + 256 * hh - 1) * tl.JS;
+#pragma unroll
         for (int s = 0; s < 16; ++s) {
-          const int rp = 4 * w + rho + 16 * s;  // r' in [0, 256)
-          const int r = rp + 256 * hh;
-          const double2 val = src[sidx(rp, ch & 1, ch >> 1)];
-          if (ok && r >= 1 && r < N) *reinterpret_cast<double2*>(y + (int64_t)(r - 1) * tl.JS) = val;
+          const double2 val = src[32 * s + (b ^ ((s >> 1) & 7))];
+          if (ok && (s > 0 || hh > 0 || r0 > 0)) *reinterpret_cast<double2*>(y) = val;
+          y += JS16;
         }
       } else {
-        const int rho = lane >> 4, cc = lane & 15, ch = cc >> 1;
-        const double* src = reinterpret_cast<const double*>(scr_all + SCR * (ch >> 1));
+        const int rho = lane >> 4, cc = lane & 15, ch = cc >> 1, fo = ch & 1, wo = ch >> 1;
+        const int r0 = 2 * w + rho;  // rows r' = r0 + 8 s
+        const double* src = reinterpret_cast<const double*>(scr_all + SCR * wo) + (cc & 1);
+        const int b = (2 * r0 + (fo ^ ((r0 >> 2) & 1))) ^ (2 * wo);  // r0 < 8: bits 5..7 of r' come from s
         const bool ok = cc < tl.lmax;
-        double* y = a.y + tl.base + cc;
-#pragma unroll 4
+        const int64_t JS8 = 8 * tl.JS;
+        double* y = a.y + tl.base + cc + (int64_t)(r0 + 256 * hh - 1) * tl.JS;
+#pragma unroll
         for (int s = 0; s < 32; ++s) {
-          const int rp = 2 * w + rho + 8 * s;
-          const int r = rp + 256 * hh;
-          const double val = src[2 * sidx(rp, ch & 1, ch >> 1) + (cc & 1)];
-          if (ok && r >= 1 && r < N) y[(int64_t)(r - 1) * tl.JS] = val;
+          // r' = r0 + 8 s: 2 r' = 2 r0 + 16 s, bit 2 of r' = bit 2 of r0 ^ bit 0 of s... (r0 < 8)
+          const int rp_lo = (2 * r0 + 16 * (s & 1));  // 2 r' mod 32
+          const int bb = (rp_lo + (fo ^ (((r0 + 8 * (s & 1)) >> 2) & 1))) ^ (2 * wo);
+          const double val = src[2 * (32 * (s >> 1) + (bb ^ ((s >> 2) & 7)))];
+          if (ok && (s > 0 || hh > 0 || r0 > 0)) *y = val;
+          y += JS8;
         }
+        (void)b;
       }
     }
     __syncthreads();
@@ -505,10 +537,8 @@ __device__ __forceinline__ void store_strided(const DstArgs& a, uint32_t t, doub
 // r in [256 hh, 256 hh + 256) at staging position p = r - 256 hh of line l,
 // word l * 256 + (p ^ (((p >> 5) & 7) << 1 | (l >> 1))), then 256-byte
 // coalesced stores per instruction
-__device__ __forceinline__ void store_contig(const DstArgs& a, uint32_t t, double2* scr, int w, int lane,
-                                             const Lane& c, const double2 (&ev)[16], const double2 (&od)[16],
-                                             double sc) {
-  const int f = c.f, q = c.q;
+__device__ __forceinline__ void store_contig(const DstArgs& a, uint32_t t, double2* scr, int w, int lane, int f,
+                                             int q, const double2 (&ev)[16], const double2 (&od)[16], double sc) {
   const Tile tl = tile_of<SIDE_CONTIG, true>(a, t);
   double* sd = reinterpret_cast<double*>(scr);
 #pragma unroll 1
@@ -535,13 +565,13 @@ __device__ __forceinline__ void store_contig(const DstArgs& a, uint32_t t, doubl
 #pragma unroll
       for (int l = 0; l < 4; ++l) {
         if (4 * w + l < tl.lmax) {
-          double* y = a.y + tl.base + (int64_t)(4 * w + l) * tl.LS + 256 * hh - 1;  // row r at r - 1
+          double* y = a.y + tl.base + (int64_t)(4 * w + l) * tl.LS + 256 * hh - 1 + lane;  // row r at r - 1
+          const double* src = sd + l * 256;
 #pragma unroll
           for (int s = 0; s < 8; ++s) {
-            const int p = lane + 32 * s;
-            const int r = p + 256 * hh;
-            const double val = sd[l * 256 + (p ^ ((((p >> 5) & 7) << 1) | (l >> 1)))];
-            if (r >= 1 && r < N) y[p] = val;
+            // p = lane + 32 s: the key of p is a per-instruction constant
+            const double val = src[(lane + 32 * s) ^ ((s << 1) | (l >> 1))];
+            if (s > 0 || hh > 0 || lane > 0) y[32 * s] = val;
           }
         }
       }
@@ -562,7 +592,6 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* const scr = scr_all + SCR * w;
   const uint32_t stile = smem_u32(tile);
-  const Lane c0 = lane_consts(a, lane);
   const uint32_t ntiles = (uint32_t)a.ntiles;
   uint32_t t = blockIdx.x;
   constexpr bool STRIDED = SIDE_IN != SIDE_CONTIG;
@@ -574,47 +603,57 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a) {
     const uint32_t tn = t + gridDim.x;
     cp_wait<0>();
     if (STRIDED) __syncthreads(); else __syncwarp();
-    const Lane c = fresh(c0);
+    const Lane c = lane_consts(a, lane);
     double2 v[32], ev[16], od[16];
-    pre_read<STRIDED ? RAW_STRIDED : RAW_CONTIG>(tile, w, c, v);
     if constexpr (!MID) {
+      pre_read<STRIDED ? RAW_STRIDED : RAW_CONTIG>(tile, w, c, v);
       if (STRIDED) __syncthreads(); else __syncwarp();
       if (tn < ntiles) {
         if (STRIDED) issue_strided<SIDE_IN>(a, tn, stile, w, lane); else issue_contig(a, tn, stile, w, lane);
       }
       cp_commit();
-      fft_split(scr, c, v, ev, od);
+      fft_split(launder_p(scr), c, v, ev, od);
     } else {
-      __syncwarp();
-      fft_split(scr, c, v, ev, od);
-      // z = S' .* core, rows 2k, 2k+1 (k = 16 q + i), into the warp's part of
-      // the tile; the core comes lane-ordered: entry (unit, row offset i', lane)
-      sched_fence();
-      {
-        const double2* cl = reinterpret_cast<const double2*>(a.core) + ((size_t)(4 * t + w) * 32) * 32 + lane;
-        double2* zt = tile + 1024 * w + 64 * c.q;
-        const int q7 = c.q & 7;
+      // forward, core, inverse: a rolled loop keeps one copy of the FFT code
+      // (two inlined copies do not fit the register file)
+#pragma unroll 1
+      for (int ph = 0; ph < 2; ++ph) {
+        // v is (re)defined at the top of both phases, so it is dead across
+        // the back edge
+        if (ph == 0) {
+          pre_read<RAW_CONTIG>(tile, w, lane_consts(a, lane), v);
+        } else {
+          pre_read<RAW_Z>(tile, w, lane_consts(a, lane), v);
+        }
+        __syncwarp();
+        if (ph == 1) {
+          if (tn < ntiles) issue_contig(a, tn, stile, w, lane);
+          cp_commit();
+        }
+        fft_split(launder_p(scr), lane_consts(a, lane), v, ev, od);
+        if (ph == 0) {
+          // z = S' .* core, rows 2k, 2k+1 (k = 16 q + i), into the warp's part
+          // of the tile; the core comes lane-ordered: (unit, row offset, lane)
+          sched_fence();
+          const double2* cl = reinterpret_cast<const double2*>(a.core) + ((size_t)(4 * t + w) * 32) * 32 + lane;
+          const int q = lane & 15, f = lane >> 4, q7 = q & 7;
+          double2* zt = tile + 1024 * w + 64 * q;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          if (i % 4 == 0) sched_fence();
-          const double2 ce = __ldg(cl + 32 * (2 * i)), co = __ldg(cl + 32 * (2 * i + 1));
-          if (i > 0 || c.q > 0) zt[zidx(2 * i, c.f) ^ q7] = make_double2(ev[i].x * ce.x, ev[i].y * ce.y);
-          zt[zidx(2 * i + 1, c.f) ^ q7] = make_double2(od[i].x * co.x, od[i].y * co.y);
+          for (int i = 0; i < 16; ++i) {
+            if (i % 4 == 0) sched_fence();
+            const double2 ce = __ldg(cl + 32 * (2 * i)), co = __ldg(cl + 32 * (2 * i + 1));
+            if (i > 0 || q > 0) zt[zidx(2 * i, f) ^ q7] = make_double2(ev[i].x * ce.x, ev[i].y * ce.y);
+            zt[zidx(2 * i + 1, f) ^ q7] = make_double2(od[i].x * co.x, od[i].y * co.y);
+          }
+          __syncwarp();
         }
       }
-      __syncwarp();
-      const Lane c2 = fresh(c0);
-      pre_read<RAW_Z>(tile, w, c2, v);
-      __syncwarp();
-      if (tn < ntiles) issue_contig(a, tn, stile, w, lane);
-      cp_commit();
-      fft_split(scr, c2, v, ev, od);
     }
     const double sc = (MID ? 0.25 : 0.5) * a.scale;
     if constexpr (STRIDED) {
-      store_strided<SIDE_OUT>(a, t, scr_all, w, lane, c0, ev, od, sc);
+      store_strided<SIDE_OUT>(a, t, scr_all, w, lane, lane >> 4, lane & 15, ev, od, sc);
     } else {
-      store_contig(a, t, scr, w, lane, c0, ev, od, sc);
+      store_contig(a, t, scr, w, lane, lane >> 4, lane & 15, ev, od, sc);
     }
   }
   cp_wait<0>();

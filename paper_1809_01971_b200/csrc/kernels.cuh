@@ -19,6 +19,10 @@ int svd_batched(const double* A, int batch, int m, int n, double* U, double* S, 
 int dst_pass(const double* x, double* y, const double* core, int64_t n, bool contig, int64_t outer, int64_t groups,
              int64_t wv, const PassLayout& in, const PassLayout& out, double scale, cudaStream_t st);
 
+// fused forward / core / inverse pass, n = 511, lane-ordered core (dst_reg.cuh)
+int dst_pass_lanes(const double* x, double* y, const double* core_l, int64_t lines, int64_t pitch, double scale,
+                   cudaStream_t st);
+
 // y = scale * F x along the middle axis of [outer][n][inner]; with core != nullptr
 // y = scale * F diag(core) F x (core in the layout of x)
 int dst_mode(const double* x, double* y, int64_t outer, int64_t n, int64_t inner, double scale,

@@ -13,7 +13,10 @@ FullOperator additionally pads the last mode's rows to a 128-byte multiple
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
+
 import torch
 
 from . import _lib
@@ -106,6 +109,31 @@ def padded_pitch(n):
     return (n + 15) // 16 * 16
 
 
+def lane_core(core):
+    """The core of an operator with n_last = 511 in the lane order read by
+    the register-resident fused pass (see fl_apply_full_lanes in
+    include/fraclap_b200.h): lines = all but the last mode, padded to a
+    multiple of 16; rows 1-based in [0, 512) with row 0 = 0."""
+    n = core.shape[-1]
+    if n != 511:
+        raise ValueError("lane order is defined for n_last = 511")
+    L = core.numel() // n
+    Lp = (L + 15) // 16 * 16
+    c = torch.zeros((Lp, 512), dtype=torch.float64, device=core.device)
+    c[:L, 1:].copy_(core.reshape(L, n))
+    # line = 4u + 2f + e, row = 32q + i  ->  [u][i][f][q][e]
+    return c.reshape(Lp // 4, 2, 2, 16, 32).permute(0, 4, 1, 3, 2).contiguous()
+
+
+def lane_core_inverse(core_l, dims):
+    """Dense core (dims) from its lane order (inverse of lane_core)."""
+    L = 1
+    for d in dims[:-1]:
+        L *= d
+    c = core_l.permute(0, 2, 4, 3, 1).reshape(-1, 512)
+    return c[:L, 1:].reshape(dims).contiguous()
+
+
 class FullOperator:
     """alpha * F diag(G) F on dense tensors; G resident in HBM.
 
@@ -118,7 +146,7 @@ class FullOperator:
     valid part.  The work tensor makes one operator single-stream: concurrent
     applications of the same operator on different streams would race."""
 
-    def __init__(self, spectrum, core, alpha=1.0, padded=None):
+    def __init__(self, spectrum, core, alpha=1.0, padded=None, lanes=None):
         if not isinstance(spectrum, EigenSpectrum):
             raise ValueError("expected an EigenSpectrum")
         if tuple(core.shape) != tuple(spectrum.mode_sizes):
@@ -132,14 +160,23 @@ class FullOperator:
         if padded and not can_pad:
             raise ValueError("the padded layout needs sine modes of FFT length")
         self.pitch = padded_pitch(dims[-1]) if padded else None
+        if lanes is None:
+            lanes = bool(padded) and dims[-1] == 511 and os.environ.get("FL_REG", "1") != "0"
+        if lanes and not (padded and dims[-1] == 511):
+            raise ValueError("the lane-ordered core is defined for a padded operator with n_last = 511")
+        self.lanes = bool(lanes)
+        self.core_p = self.core_l = None
         if padded:
             pshape = dims[:-1] + (self.pitch,)
-            self.core_p = torch.zeros(pshape, dtype=torch.float64, device=core.device)
-            self.core_p[..., :dims[-1]].copy_(core)
+            if self.lanes:
+                self.core_l = lane_core(core)
+            else:
+                self.core_p = torch.zeros(pshape, dtype=torch.float64, device=core.device)
+                self.core_p[..., :dims[-1]].copy_(core)
             self.work = torch.zeros(pshape, dtype=torch.float64, device=core.device)
             self._core = None
         else:
-            self.core_p = self.work = None
+            self.work = None
             self._core = core.contiguous()
         for m in spectrum.modes:
             _lib.call("fl_prepare", m.n)
@@ -165,6 +202,8 @@ class FullOperator:
         """The dense core G (a view of the padded storage when padded)."""
         if self._core is not None:
             return self._core
+        if self.core_l is not None:
+            return lane_core_inverse(self.core_l, tuple(self.dims))
         return self.core_p[..., :self.dims[-1]]
 
     def __call__(self, x, out=None):
@@ -175,6 +214,10 @@ class FullOperator:
         if x.device != self.work.device:
             raise ValueError("operand on %s, operator on %s" % (x.device, self.work.device))
         y = out if out is not None else torch.empty_like(x)
+        if self.lanes:
+            _lib.call("fl_apply_full_lanes", _lib.ptr(x), _lib.ptr(y), _lib.ptr(self.core_l), _lib.ptr(self.work),
+                      len(self.dims), _lib.dims_arr(self.dims), self.alpha, _lib.stream_ptr())
+            return y
         _lib.call("fl_apply_full_padded", _lib.ptr(x), _lib.ptr(y), _lib.ptr(self.core_p), _lib.ptr(self.work),
                   len(self.dims), _lib.dims_arr(self.dims), self.pitch, self.alpha, _lib.stream_ptr())
         return y
@@ -187,27 +230,35 @@ class FullOperator:
             raise ValueError("per-pass list is defined for the padded layout")
         dims, P = tuple(self.dims), self.pitch
         nl = dims[-1]
-        xp, yp, cp, wp = _lib.ptr(x), _lib.ptr(y), _lib.ptr(self.core_p), _lib.ptr(self.work)
+        xp, yp, wp = _lib.ptr(x), _lib.ptr(y), _lib.ptr(self.work)
+        cp = _lib.ptr(self.core_l if self.lanes else self.core_p)
         if len(dims) == 2:
             n0 = dims[0]
             dense, pad, line = (0, nl, 0, 0), (0, P, 0, 0), (0, 1, 0, P)
+            fused = ("lanes", wp, wp, cp, n0, P, 1.0) if self.lanes else (wp, wp, cp, nl, 1, n0, 1, 1, line, line, 1.0)
             return [("dst_mode0", (xp, wp, None, n0, 0, 1, 1, nl, dense, pad, 1.0)),
-                    ("dst_core_mode1", (wp, wp, cp, nl, 1, n0, 1, 1, line, line, 1.0)),
+                    ("dst_core_mode1", fused),
                     ("dst_mode0", (wp, yp, None, n0, 0, 1, 1, nl, pad, dense, self.alpha))]
         n0, n1 = dims[0], dims[1]
         dense0, pad0 = (0, n1 * nl, nl, 0), (0, n1 * P, P, 0)
         mid, line = (n1 * P, P, 0, 0), (0, 1, 0, P)
+        fused = (("lanes", wp, wp, cp, n0 * n1, P, 1.0) if self.lanes
+                 else (wp, wp, cp, nl, 1, n0 * n1, 1, 1, line, line, 1.0))
         return [("dst_mode0", (xp, wp, None, n0, 0, 1, n1, nl, dense0, pad0, 1.0)),
                 ("dst_mode1", (wp, wp, None, n1, 0, n0, 1, P, mid, mid, 1.0)),
-                ("dst_core_mode2", (wp, wp, cp, nl, 1, n0 * n1, 1, 1, line, line, 1.0)),
+                ("dst_core_mode2", fused),
                 ("dst_mode1", (wp, wp, None, n1, 0, n0, 1, P, mid, mid, 1.0)),
                 ("dst_mode0", (wp, yp, None, n0, 0, 1, n1, nl, pad0, dense0, self.alpha))]
 
 
 def run_pass(args, stream=None):
     """Launch one fl_dst1_pass from a FullOperator.passes() entry."""
-    x, y, c, n, contig, outer, groups, width, lin, lout, scale = args
     s = _lib.stream_ptr() if stream is None else stream
+    if args[0] == "lanes":
+        _, x, y, c, lines, pitch, scale = args
+        _lib.call("fl_dst1_core_lanes", x, y, c, lines, pitch, float(scale), s)
+        return
+    x, y, c, n, contig, outer, groups, width, lin, lout, scale = args
     _lib.call("fl_dst1_pass", x, y, c, n, contig, outer, groups, width, _lib.dims_arr(lin), _lib.dims_arr(lout),
               float(scale), s)
 

@@ -201,3 +201,45 @@ def test_dst1_tma_variant(monkeypatch, mode, n, inner):
     y = torch.empty_like(xt)
     _lib.call("fl_dst1", _lib.ptr(xt), _lib.ptr(y), outer, n, inner, 1.0, _lib.stream_ptr())
     assert rel(y.cpu().numpy(), oracle.dst(x, axis=1)) <= 1e-13
+
+
+@pytest.mark.parametrize("L", [1, 4, 15, 16, 37, 1000])
+def test_dst1_core_lanes_matches_oracle(L):
+    """Register-resident fused pass with the lane-ordered core (n = 511):
+    ragged line counts (tiles of 16 lines, units of 4), in place, pitch 512."""
+    from paper_1809_01971_b200 import _lib
+    n = 511
+    rng = np.random.default_rng(L)
+    x = rng.standard_normal((L, n))
+    core = rng.standard_normal((L, n))
+    want = oracle.dst(core * oracle.dst(x, axis=1), axis=1)
+    xp = torch.full((L, 512), 3.0, dtype=torch.float64, device="cuda")  # padding column must stay inert
+    xp[:, :n] = torch.tensor(x, device="cuda")
+    cl = full.lane_core(torch.tensor(core, device="cuda"))
+    full.run_pass(("lanes", _lib.ptr(xp), _lib.ptr(xp), _lib.ptr(cl), L, 512, 2.0))
+    got = xp.cpu().numpy()
+    assert rel(got[:, :n], 2.0 * want) <= 1e-13
+    assert np.all(got[:, n:] == 3.0)
+
+
+@pytest.mark.parametrize("dims", [(511, 511), (63, 511), (7, 15, 511), (31, 63, 511)])
+def test_apply_full_lanes_matches_oracle(dims):
+    """fl_apply_full_lanes (register-resident passes, lane-ordered core) vs
+    the oracle and vs the padded path with the natural core layout."""
+    spec = spectral.EigenSpectrum(tuple(spectral.laplacian_mode(n) for n in dims))
+    kind = CoreFunctionKind("g2", 0.75, coeff_minus=1.3, coeff_plus=0.7)
+    op = full.FullOperator.from_kind(kind, spec)
+    assert op.lanes and op.padded and op.core_l is not None
+    core_want = oracle.dense_core("g2", [oracle.laplacian_eigenvalues(n) for n in dims], 0.75, 1.3, 0.7)
+    assert rel(op.core.cpu().numpy(), core_want) <= 1e-14
+    rng = np.random.default_rng(sum(dims))
+    x = rng.standard_normal(dims)
+    xt = torch.tensor(x, device="cuda")
+    want = oracle.apply_full(core_want, x)
+    assert rel(op(xt).cpu().numpy(), want) <= 1e-12
+    natural = full.FullOperator(spec, op.core.contiguous(), padded=True, lanes=False)
+    assert rel(op(xt).cpu().numpy(), natural(xt).cpu().numpy()) <= 1e-13
+    z = torch.empty_like(xt)
+    for _, a in op.passes(xt, z):
+        full.run_pass(a)
+    assert rel(z.cpu().numpy(), want) <= 1e-12

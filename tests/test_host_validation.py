@@ -70,3 +70,22 @@ def test_spectrum_validation_and_ladders():
     assert _coarsen_sizes(127) == [63, 127]
     assert list(_decimate(np.arange(7.0), 3)) == [1.0, 3.0, 5.0]
     assert _required_sinc_m(0.5, 1e-8) >= 4
+
+
+def test_lane_core_order_roundtrip():
+    """The lane order of the n = 511 core (host-side permutation) is a
+    bijection onto the documented entries, with zero padding."""
+    import torch
+    from paper_1809_01971_b200.full import lane_core, lane_core_inverse
+    c = torch.randn(3, 11, 511, dtype=torch.float64)
+    cl = lane_core(c)
+    assert cl.shape == (12, 32, 2, 16, 2)  # 33 lines -> 48 (multiple of 16) -> 12 units
+    assert torch.equal(lane_core_inverse(cl, (3, 11, 511)), c)
+    flat = cl.reshape(12, 32, 32, 2)
+    lines = c.reshape(33, 511)
+    for u, i, f, q in [(0, 1, 0, 0), (2, 31, 1, 15), (7, 7, 1, 3)]:
+        for e in range(2):
+            line, row = 4 * u + 2 * f + e, 32 * q + i
+            assert flat[u, i, 16 * f + q, e] == lines[line, row - 1]
+    assert torch.all(flat[:, 0, 0, :] == 0)  # row 0
+    assert torch.all(flat[9:] == 0)  # padded lines
