@@ -40,6 +40,9 @@ constexpr int BUF = 1024;  // double2 per warp buffer (16 KB): 512 rows x 2 FFTs
 #define FL_REG_PRE_BATCH 8
 #endif
 constexpr int PRE_BATCH = FL_REG_PRE_BATCH;
+#ifndef FL_REG_PRE_LAUNDER
+#define FL_REG_PRE_LAUNDER 0
+#endif
 
 // unit sides: 16-byte line pairs on a strided layout, single lines on a
 // strided layout, contiguous lines with an even pitch
@@ -298,9 +301,12 @@ __device__ __forceinline__ T* launder_p(T* p) {
 
 // lane constants, re-derived per tile (lane index laundered: the smem
 // offsets computed from q are loop-invariant too)
+// (LAUNDER: the fused pass, whose larger live state otherwise spills the
+// hoisted offsets; the plain passes are faster without)
+template <bool LAUNDER = false>
 __device__ __forceinline__ Lane lane_consts(const DstArgs& a, int lane_in) {
   Lane c;
-  const int lane = launder_i(lane_in);
+  const int lane = LAUNDER ? launder_i(lane_in) : lane_in;
   c.f = lane >> 4;
   c.q = lane & 15;
   c.sq = ld_opaque(a.sn + c.q);
@@ -332,8 +338,10 @@ __device__ __forceinline__ void pre_read(const double2* tile, int w, const Lane&
   auto batch = [&](int m) {
     if (m % PRE_BATCH == 0) {
       sched_fence();
-      c.sq = launder_d(c.sq);
-      c.cq = launder_d(c.cq);
+      if (RAW != RAW_STRIDED || FL_REG_PRE_LAUNDER) {
+        c.sq = launder_d(c.sq);
+        c.cq = launder_d(c.cq);
+      }
     }
   };
   if constexpr (RAW == RAW_CONTIG) {
@@ -603,16 +611,16 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a) {
     const uint32_t tn = t + gridDim.x;
     cp_wait<0>();
     if (STRIDED) __syncthreads(); else __syncwarp();
-    const Lane c = lane_consts(a, lane);
     double2 v[32], ev[16], od[16];
     if constexpr (!MID) {
+      const Lane c = lane_consts(a, lane);
       pre_read<STRIDED ? RAW_STRIDED : RAW_CONTIG>(tile, w, c, v);
       if (STRIDED) __syncthreads(); else __syncwarp();
       if (tn < ntiles) {
         if (STRIDED) issue_strided<SIDE_IN>(a, tn, stile, w, lane); else issue_contig(a, tn, stile, w, lane);
       }
       cp_commit();
-      fft_split(launder_p(scr), c, v, ev, od);
+      fft_split(scr, c, v, ev, od);
     } else {
       // forward, core, inverse: a rolled loop keeps one copy of the FFT code
       // (two inlined copies do not fit the register file)
@@ -621,16 +629,16 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a) {
         // v is (re)defined at the top of both phases, so it is dead across
         // the back edge
         if (ph == 0) {
-          pre_read<RAW_CONTIG>(tile, w, lane_consts(a, lane), v);
+          pre_read<RAW_CONTIG>(tile, w, lane_consts<true>(a, lane), v);
         } else {
-          pre_read<RAW_Z>(tile, w, lane_consts(a, lane), v);
+          pre_read<RAW_Z>(tile, w, lane_consts<true>(a, lane), v);
         }
         __syncwarp();
         if (ph == 1) {
           if (tn < ntiles) issue_contig(a, tn, stile, w, lane);
           cp_commit();
         }
-        fft_split(launder_p(scr), lane_consts(a, lane), v, ev, od);
+        fft_split(launder_p(scr), lane_consts<true>(a, lane), v, ev, od);
         if (ph == 0) {
           // z = S' .* core, rows 2k, 2k+1 (k = 16 q + i), into the warp's part
           // of the tile; the core comes lane-ordered: (unit, row offset, lane)
