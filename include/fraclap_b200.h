@@ -139,7 +139,14 @@ int fl_dst1_core_lanes(const double* x, double* y, const double* core_l, int64_t
  * column groups of `width` columns, element (block o, group g, column c,
  * row j) at o*os + g*gp + c + j*js.  in_layout / out_layout are int64[4]
  * {os, js, gp, lp} for x (and core) / y.  core != NULL (contig only) runs
- * the fused forward-scale-inverse pass.  FFT lengths only. */
+ * the fused forward-scale-inverse pass.  FFT lengths only.  `contig` is a
+ * flag word: FL_PASS_CONTIG selects contiguous lines; FL_PASS_PAD_WRITE
+ * lets a strided pass with an odd width write the column after each group
+ * (the padding of an internal work buffer, as in fl_apply_full_padded)
+ * so that it can store 16-byte line pairs; without it the padding is never
+ * written. */
+#define FL_PASS_CONTIG 1
+#define FL_PASS_PAD_WRITE 2
 int fl_dst1_pass(const double* x, double* y, const double* core, int64_t n, int contig,
                  int64_t outer, int64_t groups, int64_t width, const int64_t* in_layout,
                  const int64_t* out_layout, double scale, void* stream);

@@ -130,14 +130,14 @@ int fl_apply_full_padded(const double* x, double* y, const double* core_p, doubl
   if (d == 2) {
     const int64_t n0 = dims[0];
     const PassLayout dense{0, nl, 0, 0}, padded{0, P, 0, 0};
-    if ((rc = dst_pass(x, work, nullptr, n0, false, 1, 1, nl, dense, padded, 1.0, st))) return rc;
+    if ((rc = dst_pass(x, work, nullptr, n0, false, 1, 1, nl, dense, padded, 1.0, st, true))) return rc;
     if ((rc = dst_pass(work, work, core_p, nl, true, n0, 1, 1, line, line, 1.0, st))) return rc;
     return dst_pass(work, y, nullptr, n0, false, 1, 1, nl, padded, dense, alpha, st);
   }
   const int64_t n0 = dims[0], n1 = dims[1];
   const PassLayout dense0{0, n1 * nl, nl, 0}, padded0{0, n1 * P, P, 0};
   const PassLayout mid{n1 * P, P, 0, 0};
-  if ((rc = dst_pass(x, work, nullptr, n0, false, 1, n1, nl, dense0, padded0, 1.0, st))) return rc;
+  if ((rc = dst_pass(x, work, nullptr, n0, false, 1, n1, nl, dense0, padded0, 1.0, st, true))) return rc;
   if ((rc = dst_pass(work, work, nullptr, n1, false, n0, 1, P, mid, mid, 1.0, st))) return rc;
   if ((rc = dst_pass(work, work, core_p, nl, true, n0 * n1, 1, 1, line, line, 1.0, st))) return rc;
   if ((rc = dst_pass(work, work, nullptr, n1, false, n0, 1, P, mid, mid, 1.0, st))) return rc;
@@ -157,14 +157,14 @@ int fl_apply_full_lanes(const double* x, double* y, const double* core_l, double
   if (d == 2) {
     const int64_t n0 = dims[0];
     const PassLayout dense{0, nl, 0, 0}, padded{0, P, 0, 0};
-    if ((rc = dst_pass(x, work, nullptr, n0, false, 1, 1, nl, dense, padded, 1.0, st))) return rc;
+    if ((rc = dst_pass(x, work, nullptr, n0, false, 1, 1, nl, dense, padded, 1.0, st, true))) return rc;
     if ((rc = dst_pass_lanes(work, work, core_l, n0, P, 1.0, st))) return rc;
     return dst_pass(work, y, nullptr, n0, false, 1, 1, nl, padded, dense, alpha, st);
   }
   const int64_t n0 = dims[0], n1 = dims[1];
   const PassLayout dense0{0, n1 * nl, nl, 0}, padded0{0, n1 * P, P, 0};
   const PassLayout mid{n1 * P, P, 0, 0};
-  if ((rc = dst_pass(x, work, nullptr, n0, false, 1, n1, nl, dense0, padded0, 1.0, st))) return rc;
+  if ((rc = dst_pass(x, work, nullptr, n0, false, 1, n1, nl, dense0, padded0, 1.0, st, true))) return rc;
   if ((rc = dst_pass(work, work, nullptr, n1, false, n0, 1, P, mid, mid, 1.0, st))) return rc;
   if ((rc = dst_pass_lanes(work, work, core_l, n0 * n1, P, 1.0, st))) return rc;
   if ((rc = dst_pass(work, work, nullptr, n1, false, n0, 1, P, mid, mid, 1.0, st))) return rc;
@@ -182,7 +182,8 @@ int fl_dst1_pass(const double* x, double* y, const double* core, int64_t n, int 
   FL_ARG_CHECK(in_layout != nullptr && out_layout != nullptr, "layouts required");
   const PassLayout in{in_layout[0], in_layout[1], in_layout[2], in_layout[3]};
   const PassLayout out{out_layout[0], out_layout[1], out_layout[2], out_layout[3]};
-  return dst_pass(x, y, core, n, contig != 0, outer, groups, width, in, out, scale, as_stream(stream));
+  return dst_pass(x, y, core, n, (contig & FL_PASS_CONTIG) != 0, outer, groups, width, in, out, scale,
+                  as_stream(stream), (contig & FL_PASS_PAD_WRITE) != 0);
 }
 
 int fl_transform_full(const double* x, double* y, int d, const int64_t* dims, double alpha, void* stream) {

@@ -318,7 +318,7 @@ int dispatch_fft(int logn, const DstArgs& a, cudaStream_t st) {
 // One DST-I pass with explicit input/output layouts (see DstArgs).  FFT
 // lengths only; the standard [outer][n][inner] pass is dst_mode below.
 int dst_pass(const double* x, double* y, const double* core, int64_t n, bool contig, int64_t outer, int64_t groups,
-             int64_t wv, const PassLayout& in, const PassLayout& out, double scale, cudaStream_t st) {
+             int64_t wv, const PassLayout& in, const PassLayout& out, double scale, cudaStream_t st, bool pad_write) {
   FL_ARG_CHECK(n >= 1 && outer >= 0 && groups >= 1 && wv >= 0, "bad DST pass shape");
   FL_ARG_CHECK(fft_len_ok(n), "pass layouts need an FFT length (n+1 a power of two in [4, 8192]), got %lld",
                (long long)n);
@@ -349,10 +349,17 @@ int dst_pass(const double* x, double* y, const double* core, int64_t n, bool con
   a.core = core;
   a.tw = t->tw;
   a.sn = t->sn;
-  if (!contig && wv % 2 == 0) {
+  if (!contig) {
+    // 16-byte line pairs: aligned base and strides; an odd group width is
+    // fine when the layout has room for one more column after the last
+    // (a padded row), which the pair access then touches: reads ignore it,
+    // writes (only into internal work buffers, pad_write) store the finite
+    // transform of the zero-filled partner line
     auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
-    a.vec_in = al(x) && (core == nullptr || al(core)) && in.os % 2 == 0 && in.gp % 2 == 0 && in.js % 2 == 0;
-    a.vec_out = al(y) && out.os % 2 == 0 && out.gp % 2 == 0 && out.js % 2 == 0;
+    auto room = [&](const PassLayout& l) { return wv % 2 == 0 || (groups > 1 ? l.gp > wv : l.js > wv); };
+    a.vec_in = al(x) && (core == nullptr || al(core)) && in.os % 2 == 0 && in.gp % 2 == 0 && in.js % 2 == 0 &&
+               room(in);
+    a.vec_out = al(y) && out.os % 2 == 0 && out.gp % 2 == 0 && out.js % 2 == 0 && (wv % 2 == 0 || (pad_write && room(out)));
   }
   if (logn == 9 && reg_enabled()) {
     if (core == nullptr && !contig) {

@@ -649,7 +649,8 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             if (i % 4 == 0) sched_fence();
-            const double2 ce = __ldg(cl + 32 * (2 * i)), co = __ldg(cl + 32 * (2 * i + 1));
+            const double2 ce = FL_REG_NOMEM ? make_double2(1.0, 1.0) : __ldg(cl + 32 * (2 * i));
+            const double2 co = FL_REG_NOMEM ? make_double2(1.0, 1.0) : __ldg(cl + 32 * (2 * i + 1));
             if (i > 0 || q > 0) zt[zidx(2 * i, f) ^ q7] = make_double2(ev[i].x * ce.x, ev[i].y * ce.y);
             zt[zidx(2 * i + 1, f) ^ q7] = make_double2(od[i].x * co.x, od[i].y * co.y);
           }

@@ -17,7 +17,8 @@ bool fft_length(int64_t n);
 int svd_batched(const double* A, int batch, int m, int n, double* U, double* S, double* Vt, cudaStream_t st);
 
 int dst_pass(const double* x, double* y, const double* core, int64_t n, bool contig, int64_t outer, int64_t groups,
-             int64_t wv, const PassLayout& in, const PassLayout& out, double scale, cudaStream_t st);
+             int64_t wv, const PassLayout& in, const PassLayout& out, double scale, cudaStream_t st,
+             bool pad_write = false);
 
 // fused forward / core / inverse pass, n = 511, lane-ordered core (dst_reg.cuh)
 int dst_pass_lanes(const double* x, double* y, const double* core_l, int64_t lines, int64_t pitch, double scale,

@@ -236,7 +236,8 @@ class FullOperator:
             n0 = dims[0]
             dense, pad, line = (0, nl, 0, 0), (0, P, 0, 0), (0, 1, 0, P)
             fused = ("lanes", wp, wp, cp, n0, P, 1.0) if self.lanes else (wp, wp, cp, nl, 1, n0, 1, 1, line, line, 1.0)
-            return [("dst_mode0", (xp, wp, None, n0, 0, 1, 1, nl, dense, pad, 1.0)),
+            # flag 2 = FL_PASS_PAD_WRITE: the first pass may write the work tensor's padding
+            return [("dst_mode0", (xp, wp, None, n0, 2, 1, 1, nl, dense, pad, 1.0)),
                     ("dst_core_mode1", fused),
                     ("dst_mode0", (wp, yp, None, n0, 0, 1, 1, nl, pad, dense, self.alpha))]
         n0, n1 = dims[0], dims[1]
@@ -244,7 +245,8 @@ class FullOperator:
         mid, line = (n1 * P, P, 0, 0), (0, 1, 0, P)
         fused = (("lanes", wp, wp, cp, n0 * n1, P, 1.0) if self.lanes
                  else (wp, wp, cp, nl, 1, n0 * n1, 1, 1, line, line, 1.0))
-        return [("dst_mode0", (xp, wp, None, n0, 0, 1, n1, nl, dense0, pad0, 1.0)),
+        # flag 2 = FL_PASS_PAD_WRITE: the first pass may write the work tensor's padding
+        return [("dst_mode0", (xp, wp, None, n0, 2, 1, n1, nl, dense0, pad0, 1.0)),
                 ("dst_mode1", (wp, wp, None, n1, 0, n0, 1, P, mid, mid, 1.0)),
                 ("dst_core_mode2", fused),
                 ("dst_mode1", (wp, wp, None, n1, 0, n0, 1, P, mid, mid, 1.0)),
