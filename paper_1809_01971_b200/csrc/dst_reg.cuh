@@ -634,25 +634,44 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a) {
           pre_read<RAW_Z>(tile, w, lane_consts<true>(a, lane), v);
         }
         __syncwarp();
-        if (ph == 1) {
+        if (ph == 0) {
+          // the warp's 16 KB of the tile is free: bring the unit's lane-ordered
+          // core slice there while the forward FFT runs
+          if (!FL_REG_NOMEM) {
+            const double2* cl = reinterpret_cast<const double2*>(a.core) + (size_t)(4 * t + w) * 1024 + lane;
+            const uint32_t d = stile + 16u * (uint32_t)(1024 * w + lane);
+            static_for<0, 32>([&](auto I) {
+              constexpr int i = decltype(I)::value;
+              cp16<16 * 32 * i>(d, cl + 32 * i, 16);
+            });
+          }
+          cp_commit();
+        } else {
           if (tn < ntiles) issue_contig(a, tn, stile, w, lane);
           cp_commit();
         }
-        fft_split(launder_p(scr), lane_consts<true>(a, lane), v, ev, od);
+        // shared addressing survives: the laundered part is an integer offset
+        fft_split(scr_all + launder_i(SCR * w), lane_consts<true>(a, lane), v, ev, od);
         if (ph == 0) {
-          // z = S' .* core, rows 2k, 2k+1 (k = 16 q + i), into the warp's part
-          // of the tile; the core comes lane-ordered: (unit, row offset, lane)
-          sched_fence();
-          const double2* cl = reinterpret_cast<const double2*>(a.core) + ((size_t)(4 * t + w) * 32) * 32 + lane;
+          // z = S' .* core for rows 2k, 2k+1 (k = 16 q + i): multiply in
+          // registers (core entry (i', lane) at 32 i' + lane), then write z
+          // over the core in the z layout
+          cp_wait<0>();
+          __syncwarp();
+          const double2* cw = tile + 1024 * w + lane;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const double2 ce = cw[32 * (2 * i)], co = cw[32 * (2 * i + 1)];
+            ev[i] = make_double2(ev[i].x * ce.x, ev[i].y * ce.y);
+            od[i] = make_double2(od[i].x * co.x, od[i].y * co.y);
+          }
+          __syncwarp();
           const int q = lane & 15, f = lane >> 4, q7 = q & 7;
           double2* zt = tile + 1024 * w + 64 * q;
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            if (i % 4 == 0) sched_fence();
-            const double2 ce = FL_REG_NOMEM ? make_double2(1.0, 1.0) : __ldg(cl + 32 * (2 * i));
-            const double2 co = FL_REG_NOMEM ? make_double2(1.0, 1.0) : __ldg(cl + 32 * (2 * i + 1));
-            if (i > 0 || q > 0) zt[zidx(2 * i, f) ^ q7] = make_double2(ev[i].x * ce.x, ev[i].y * ce.y);
-            zt[zidx(2 * i + 1, f) ^ q7] = make_double2(od[i].x * co.x, od[i].y * co.y);
+            if (i > 0 || q > 0) zt[zidx(2 * i, f) ^ q7] = ev[i];
+            zt[zidx(2 * i + 1, f) ^ q7] = od[i];
           }
           __syncwarp();
         }
