@@ -115,21 +115,31 @@ int fl_apply_full_padded(const double* x, double* y, const double* core_p, doubl
                          int d, const int64_t* dims, int64_t pitch, double alpha,
                          void* stream);
 
-/* Same operator for n_last = 511 (N = 512, the configs[2] grid) with the
- * core in lane order, the layout the register-resident fused pass reads
- * with one coalesced 512-byte load per warp instruction: for 4-line unit u
- * (lines 4u .. 4u+3 of the padded [line][pitch = 512] view, line = index
- * over all but the last mode), row offset i in [0, 32) and lane
- * l = 16 f + q, entry ((u * 32 + i) * 32 + l) is the double pair
- * (G[line 4u + 2f][row 32q + i], G[line 4u + 2f + 1][row 32q + i]), rows
- * 1-based (row 0 is zero); units are padded to a multiple of 4 (16 lines).
- * work as for fl_apply_full_padded (pitch 512).  d = 2 or 3. */
+/* Same operator for n_0 = n_last = 511 (N = 512, the configs[2] grid)
+ * through the register-resident passes: last mode first (contiguous dense
+ * rows into the padded work tensor), mode 1, then mode 0 forward + core +
+ * inverse in one pass, mode 1, last mode back into y.  core_l is the core
+ * in the mode-0 lane order read by the fused pass with one coalesced
+ * 512-byte load per warp instruction: with G padded to [511][n1][512]
+ * (pad column zero; n1 = 1 for d = 2), unit u = (i1 * 32 + c) * 4 + w
+ * covers columns i2 = 16c + 4w .. 16c + 4w + 3; entry ((u * 32 + i) * 32
+ * + 16 f + q) is the double pair (G[r - 1][i1][16c + 4w + 2f],
+ * G[r - 1][i1][16c + 4w + 2f + 1]), r = 32q + i (r = 0 gives zeros).
+ * work: [511][n1][512] doubles, padding zero-initialised once. */
 int fl_apply_full_lanes(const double* x, double* y, const double* core_l, double* work,
                         int d, const int64_t* dims, double alpha, void* stream);
 
-/* The fused last-mode pass of fl_apply_full_lanes on its own (per-pass
- * timing): `lines` contiguous lines of pitch `pitch` (>= 512, even),
- * y = scale * F diag(core_l) F x per line, n = 511.  x == y allowed. */
+/* The fused mode-0 pass of fl_apply_full_lanes on its own (per-pass timing):
+ * y = scale * F_0 diag(core_l) F_0 x on [511][groups][512], x == y allowed. */
+int fl_dst1_core_lanes_mode0(const double* x, double* y, const double* core_l, int64_t groups,
+                             double scale, void* stream);
+
+/* Fused pass along contiguous lines with a line-ordered core (n = 511):
+ * `lines` lines of pitch `pitch` (>= 512, even), y = scale * F diag(G) F x
+ * per line; core_l is G in the line lane order: unit u = lines 4u .. 4u+3,
+ * entry ((u * 32 + i) * 32 + 16 f + q) = (G[4u + 2f][r - 1],
+ * G[4u + 2f + 1][r - 1]), r = 32q + i, units padded to a multiple of 4.
+ * x == y allowed. */
 int fl_dst1_core_lanes(const double* x, double* y, const double* core_l, int64_t lines,
                        int64_t pitch, double scale, void* stream);
 

@@ -149,26 +149,27 @@ int fl_apply_full_lanes(const double* x, double* y, const double* core_l, double
   int rc = check_dims(d, dims);
   if (rc) return rc;
   FL_ARG_CHECK(core_l != nullptr && work != nullptr, "lane-ordered core and work buffer required");
-  FL_ARG_CHECK(dims[d - 1] == 511, "lane-ordered core needs n_last = 511, got %lld", (long long)dims[d - 1]);
+  FL_ARG_CHECK(dims[0] == 511 && dims[d - 1] == 511, "lane-ordered apply needs n_0 = n_last = 511");
   for (int l = 0; l < d; ++l)
     FL_ARG_CHECK(fft_length(dims[l]), "lane apply needs FFT lengths, mode %d has n = %lld", l, (long long)dims[l]);
-  const int64_t nl = 511, P = 512;
+  const int64_t n0 = 511, nl = 511, P = 512;
+  const int64_t n1 = d == 3 ? dims[1] : 1;
+  const int64_t lines = n0 * n1;  // lines of the last mode
   cudaStream_t st = as_stream(stream);
-  if (d == 2) {
-    const int64_t n0 = dims[0];
-    const PassLayout dense{0, nl, 0, 0}, padded{0, P, 0, 0};
-    if ((rc = dst_pass(x, work, nullptr, n0, false, 1, 1, nl, dense, padded, 1.0, st, true))) return rc;
-    if ((rc = dst_pass_lanes(work, work, core_l, n0, P, 1.0, st))) return rc;
-    return dst_pass(work, y, nullptr, n0, false, 1, 1, nl, padded, dense, alpha, st);
-  }
-  const int64_t n0 = dims[0], n1 = dims[1];
-  const PassLayout dense0{0, n1 * nl, nl, 0}, padded0{0, n1 * P, P, 0};
+  // last mode first, contiguous: dense rows (pitch 511) -> padded rows (512)
+  const PassLayout dense_l{0, 1, 0, nl}, pad_l{0, 1, 0, P};
+  if ((rc = dst_pass(x, work, nullptr, nl, true, lines, 1, 1, dense_l, pad_l, 1.0, st))) return rc;
   const PassLayout mid{n1 * P, P, 0, 0};
-  if ((rc = dst_pass(x, work, nullptr, n0, false, 1, n1, nl, dense0, padded0, 1.0, st, true))) return rc;
-  if ((rc = dst_pass(work, work, nullptr, n1, false, n0, 1, P, mid, mid, 1.0, st))) return rc;
-  if ((rc = dst_pass_lanes(work, work, core_l, n0 * n1, P, 1.0, st))) return rc;
-  if ((rc = dst_pass(work, work, nullptr, n1, false, n0, 1, P, mid, mid, 1.0, st))) return rc;
-  return dst_pass(work, y, nullptr, n0, false, 1, n1, nl, padded0, dense0, alpha, st);
+  if (d == 3 && (rc = dst_pass(work, work, nullptr, n1, false, n0, 1, P, mid, mid, 1.0, st))) return rc;
+  // mode 0: forward, core, inverse in one pass
+  if ((rc = dst_pass_lanes_mode0(work, work, core_l, n1, 1.0, st))) return rc;
+  if (d == 3 && (rc = dst_pass(work, work, nullptr, n1, false, n0, 1, P, mid, mid, 1.0, st))) return rc;
+  return dst_pass(work, y, nullptr, nl, true, lines, 1, 1, pad_l, dense_l, alpha, st);
+}
+
+int fl_dst1_core_lanes_mode0(const double* x, double* y, const double* core_l, int64_t groups, double scale,
+                             void* stream) {
+  return dst_pass_lanes_mode0(x, y, core_l, groups, scale, as_stream(stream));
 }
 
 int fl_dst1_core_lanes(const double* x, double* y, const double* core_l, int64_t lines, int64_t pitch, double scale,

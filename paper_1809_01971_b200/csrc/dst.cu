@@ -362,6 +362,11 @@ int dst_pass(const double* x, double* y, const double* core, int64_t n, bool con
     a.vec_out = al(y) && out.os % 2 == 0 && out.gp % 2 == 0 && out.js % 2 == 0 && (wv % 2 == 0 || (pad_write && room(out)));
   }
   if (logn == 9 && reg_enabled()) {
+    auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+    if (core == nullptr && contig && in.lp >= 511 && al16(x)) {
+      a.scale = scale * nrm;
+      return launch_reg<rg::SIDE_CONTIG, rg::SIDE_CONTIG, false>(a, st);
+    }
     if (core == nullptr && !contig) {
       a.scale = scale * nrm;
       if (a.vec_in && a.vec_out) return launch_reg<rg::SIDE_VEC, rg::SIDE_VEC, false>(a, st);
@@ -392,6 +397,34 @@ int dst_pass(const double* x, double* y, const double* core, int64_t n, bool con
 }
 
 bool fft_length(int64_t n) { return fft_len_ok(n); }
+
+int dst_pass_lanes_mode0(const double* x, double* y, const double* core_l, int64_t groups, double scale,
+                         cudaStream_t st) {
+  FL_ARG_CHECK(x != nullptr && y != nullptr && core_l != nullptr, "null pointer");
+  FL_ARG_CHECK(groups >= 1, "lane-core mode-0 pass: groups must be >= 1");
+  auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  FL_ARG_CHECK(al(x) && al(y) && al(core_l), "lane-core pass: 16-byte aligned buffers required");
+  const Tables* t = nullptr;
+  int rc = get_tables(511, &t);
+  if (rc) return rc;
+  const double nrm = std::sqrt(2.0 / 512.0);
+  DstArgs a{};
+  a.x = x;
+  a.y = y;
+  a.outer = 1;
+  a.n = 511;
+  a.groups = groups;
+  a.wv = 512;
+  a.in_os = a.out_os = 0;
+  a.in_js = a.out_js = groups * 512;
+  a.in_gp = a.out_gp = 512;
+  a.vec_in = a.vec_out = 1;
+  a.core = core_l;
+  a.tw = t->tw;
+  a.sn = t->sn;
+  a.scale = scale * nrm * nrm;
+  return launch_reg<rg::SIDE_VEC, rg::SIDE_VEC, true>(a, st);
+}
 
 int dst_pass_lanes(const double* x, double* y, const double* core_l, int64_t lines, int64_t pitch, double scale,
                    cudaStream_t st) {

@@ -214,7 +214,7 @@ __device__ __forceinline__ void static_for(F&& f) {
 // instruction covers 4 (16-byte side) or 2 (8-byte side) whole row segments)
 template <int SIDE>
 __device__ __forceinline__ void issue_strided(const DstArgs& a, uint32_t t, uint32_t stile, int w, int lane) {
-  if (FL_REG_NOMEM) return;
+  if (FL_REG_NOMEM == 1 || FL_REG_NOMEM == 2) return;
   const Tile tl = tile_of<SIDE, false>(a, t);
   if constexpr (SIDE == SIDE_VEC) {
     const int rho = lane >> 3, c = lane & 7;
@@ -244,18 +244,28 @@ __device__ __forceinline__ void issue_strided(const DstArgs& a, uint32_t t, uint
   }
 }
 
-// cp.async loads of warp w's 4 lines of contiguous tile t ([line][512])
+// cp.async loads of warp w's 4 lines of contiguous tile t ([line][512]).
+// A line whose start is not 16-byte aligned (odd pitch, e.g. the dense
+// 511-pitch tensor) is copied from one element earlier: row j sits at
+// position j - 1 + shift, shift = parity of the line's element offset.  The
+// last chunk of an aligned line reads only its first element (the second
+// would be past the line, possibly past the tensor).
+__device__ __forceinline__ int line_shift(const Tile& tl, int l) { return (int)((tl.base + l * tl.LS) & 1); }
+
 __device__ __forceinline__ void issue_contig(const DstArgs& a, uint32_t t, uint32_t stile, int w, int lane) {
-  if (FL_REG_NOMEM) return;
+  if (FL_REG_NOMEM == 1 || FL_REG_NOMEM == 2) return;
   const Tile tl = tile_of<SIDE_CONTIG, false>(a, t);
   const uint32_t d = stile + 8u * (uint32_t)(4 * w * 512) + 16u * (uint32_t)lane;
   static_for<0, 4>([&](auto L) {
     constexpr int l = decltype(L)::value;
-    const int sz = 4 * w + l < tl.lmax ? 16 : 0;
-    const double* src = a.x + tl.base + (int64_t)(4 * w + l) * tl.LS + 2 * lane;
+    const bool ok = 4 * w + l < tl.lmax;
+    const int sh = line_shift(tl, 4 * w + l);
+    const double* src = ok ? a.x + tl.base + (int64_t)(4 * w + l) * tl.LS - sh + 2 * lane : a.x;
+    const int sz = ok ? 16 : 0;
+    const int szl = ok ? (sh ? 16 : (lane == 31 ? 8 : 16)) : 0;
     static_for<0, 8>([&](auto I) {
       constexpr int i = decltype(I)::value;
-      cp16<8 * (l * 512 + 64 * i)>(d, sz ? src + 64 * i : a.x, sz);
+      cp16<8 * (l * 512 + 64 * i)>(d, ok ? src + 64 * i : a.x, i == 7 ? szl : sz);
     });
   });
 }
@@ -330,7 +340,8 @@ __device__ __forceinline__ double2 pre_y(const Lane& c, int m, double2 xa, doubl
 
 // pre-processed input y_{q + 16 m} of FFT f of warp w
 template <int RAW>
-__device__ __forceinline__ void pre_read(const double2* tile, int w, const Lane& c_in, double2 (&v)[32]) {
+__device__ __forceinline__ void pre_read(const double2* tile, int w, const Lane& c_in, double2 (&v)[32], int sha = 0,
+                                         int shb = 0) {
   Lane c = c_in;
   const int f = c.f, q = c.q, q7 = q & 7;
   // each batch's sines are computed from freshly laundered sin/cos, so the
@@ -345,15 +356,17 @@ __device__ __forceinline__ void pre_read(const double2* tile, int w, const Lane&
     }
   };
   if constexpr (RAW == RAW_CONTIG) {
+    // lines 4w + 2f (real) and 4w + 2f + 1 (imag), row j at j - 1 + shift
     const double* d = reinterpret_cast<const double*>(tile) + (4 * w + 2 * f) * 512;
-    const double* pa = d + q - 1;    // row j at j - 1
-    const double* pb = d + 511 - q;  // row N - j, j = q + 16 m
+    const double* ra = d + sha - 1;
+    const double* rb = d + 512 + shb - 1;
 #pragma unroll
     for (int m = 0; m < 32; ++m) {
       batch(m);
-      const double* qa = (m == 0) ? (q == 0 ? pb : pa) : pa + 16 * m;
-      const double* qb = pb - 16 * m;
-      v[m] = pre_y(c, m, make_double2(qa[0], qa[512]), make_double2(qb[0], qb[512]));
+      const int j = (m == 0) ? (q == 0 ? 1 : q) : q + 16 * m;  // q + 16 m (row 0 -> any valid row)
+      const int jp = 512 - q - 16 * m;                         // N - j (m = 0, q = 0: 512 -> clamp)
+      const int jb = (m == 0 && q == 0) ? 1 : jp;
+      v[m] = pre_y(c, m, make_double2(ra[j], rb[j]), make_double2(ra[jb], rb[jb]));
     }
   } else if constexpr (RAW == RAW_STRIDED) {
     const int ch = 2 * w + f;
@@ -482,6 +495,44 @@ __device__ __forceinline__ void fft_split(double2* scr, const Lane& c, double2 (
 // in its warp's scratch, then the CTA writes whole row segments.  Row
 // r' = r0 + 16 s of the half (r0 = 4w + rho lane-constant) sits at
 // sidx(r', f', w') = 32 s + (b ^ ((s >> 1) & 7)) with b lane-constant.
+#ifndef FL_REG_DIRECT_STORE
+#define FL_REG_DIRECT_STORE 0
+#endif
+// strided output straight from registers: lane (f, q) writes rows 32q + 2i
+// (+1) of its line pair, 16 bytes per row; a warp instruction covers 16 rows
+// x 32 bytes (sector-complete), no staging and no CTA barrier
+template <int SIDE_OUT>
+__device__ __forceinline__ void store_strided_direct(const DstArgs& a, uint32_t t, int w, int f, int q,
+                                                     const double2 (&ev)[16], const double2 (&od)[16], double sc) {
+  const Tile tl = tile_of<SIDE_OUT, true>(a, t);
+  const int col = 4 * w + 2 * f;
+  const bool va = col < tl.lmax, vb = col + 1 < tl.lmax;
+  double* p = a.y + tl.base + col + (int64_t)(32 * q) * tl.JS;  // odd row 32q + 2i + 1 at 32q + 2i
+  const int64_t JS = tl.JS, JS2 = 2 * tl.JS;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const double2 e = make_double2(sc * ev[i].x, sc * ev[i].y);
+    const double2 o = make_double2(sc * od[i].x, sc * od[i].y);
+    double* pe = p - JS;
+    if (SIDE_OUT == SIDE_VEC) {
+      if (va) {
+        if (i > 0 || q > 0) *reinterpret_cast<double2*>(pe) = e;
+        *reinterpret_cast<double2*>(p) = o;
+      }
+    } else {
+      if (va) {
+        if (i > 0 || q > 0) pe[0] = e.x;
+        p[0] = o.x;
+      }
+      if (vb) {
+        if (i > 0 || q > 0) pe[1] = e.y;
+        p[1] = o.y;
+      }
+    }
+    p += JS2;
+  }
+}
+
 template <int SIDE_OUT>
 __device__ __forceinline__ void store_strided(const DstArgs& a, uint32_t t, double2* scr_all, int w, int lane, int f,
                                               int q, const double2 (&ev)[16], const double2 (&od)[16], double sc) {
@@ -502,7 +553,7 @@ __device__ __forceinline__ void store_strided(const DstArgs& a, uint32_t t, doub
       }
     }
     __syncthreads();
-    if (!FL_REG_NOMEM || a.scale == 12345.0) {
+    if (!(FL_REG_NOMEM == 1 || FL_REG_NOMEM == 3) || a.scale == 12345.0) {
       if constexpr (SIDE_OUT == SIDE_VEC) {
         const int rho = lane >> 3, ch = lane & 7, fo = ch & 1, wo = ch >> 1;
         const int r0 = 4 * w + rho;  // rows r' = r0 + 16 s
@@ -569,7 +620,7 @@ __device__ __forceinline__ void store_contig(const DstArgs& a, uint32_t t, doubl
       }
     }
     __syncwarp();
-    if (!FL_REG_NOMEM || a.scale == 12345.0) {
+    if (!(FL_REG_NOMEM == 1 || FL_REG_NOMEM == 3) || a.scale == 12345.0) {
 #pragma unroll
       for (int l = 0; l < 4; ++l) {
         if (4 * w + l < tl.lmax) {
@@ -612,9 +663,15 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a) {
     cp_wait<0>();
     if (STRIDED) __syncthreads(); else __syncwarp();
     double2 v[32], ev[16], od[16];
+    int sha = 0, shb = 0;  // contiguous tiles: alignment shifts of the warp's lines 4w + 2f, 4w + 2f + 1
+    if constexpr (!STRIDED) {
+      const Tile tin = tile_of<SIDE_CONTIG, false>(a, t);
+      sha = line_shift(tin, 4 * w + 2 * (lane >> 4));
+      shb = line_shift(tin, 4 * w + 2 * (lane >> 4) + 1);
+    }
     if constexpr (!MID) {
       const Lane c = lane_consts(a, lane);
-      pre_read<STRIDED ? RAW_STRIDED : RAW_CONTIG>(tile, w, c, v);
+      pre_read<STRIDED ? RAW_STRIDED : RAW_CONTIG>(tile, w, c, v, sha, shb);
       if (STRIDED) __syncthreads(); else __syncwarp();
       if (tn < ntiles) {
         if (STRIDED) issue_strided<SIDE_IN>(a, tn, stile, w, lane); else issue_contig(a, tn, stile, w, lane);
@@ -629,14 +686,16 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a) {
         // v is (re)defined at the top of both phases, so it is dead across
         // the back edge
         if (ph == 0) {
-          pre_read<RAW_CONTIG>(tile, w, lane_consts<true>(a, lane), v);
+          pre_read<STRIDED ? RAW_STRIDED : RAW_CONTIG>(tile, w, lane_consts<true>(a, lane), v, sha, shb);
         } else {
           pre_read<RAW_Z>(tile, w, lane_consts<true>(a, lane), v);
         }
-        __syncwarp();
+        // phase 0: the tile is consumed, quarter w (16 KB) is the warp's own
+        // from here; phase 1: every warp has read its z, the tile is free
+        if (STRIDED) __syncthreads(); else __syncwarp();
         if (ph == 0) {
-          // the warp's 16 KB of the tile is free: bring the unit's lane-ordered
-          // core slice there while the forward FFT runs
+          // bring the unit's lane-ordered core slice into quarter w while the
+          // forward FFT runs
           if (!FL_REG_NOMEM) {
             const double2* cl = reinterpret_cast<const double2*>(a.core) + (size_t)(4 * t + w) * 1024 + lane;
             const uint32_t d = stile + 16u * (uint32_t)(1024 * w + lane);
@@ -647,7 +706,9 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a) {
           }
           cp_commit();
         } else {
-          if (tn < ntiles) issue_contig(a, tn, stile, w, lane);
+          if (tn < ntiles) {
+            if (STRIDED) issue_strided<SIDE_IN>(a, tn, stile, w, lane); else issue_contig(a, tn, stile, w, lane);
+          }
           cp_commit();
         }
         // shared addressing survives: the laundered part is an integer offset
@@ -679,7 +740,11 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a) {
     }
     const double sc = (MID ? 0.25 : 0.5) * a.scale;
     if constexpr (STRIDED) {
-      store_strided<SIDE_OUT>(a, t, scr_all, w, lane, lane >> 4, lane & 15, ev, od, sc);
+      if (FL_REG_DIRECT_STORE) {
+        store_strided_direct<SIDE_OUT>(a, t, w, lane >> 4, lane & 15, ev, od, sc);
+      } else {
+        store_strided<SIDE_OUT>(a, t, scr_all, w, lane, lane >> 4, lane & 15, ev, od, sc);
+      }
     } else {
       store_contig(a, t, scr, w, lane, lane >> 4, lane & 15, ev, od, sc);
     }

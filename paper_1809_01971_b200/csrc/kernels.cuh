@@ -24,6 +24,11 @@ int dst_pass(const double* x, double* y, const double* core, int64_t n, bool con
 int dst_pass_lanes(const double* x, double* y, const double* core_l, int64_t lines, int64_t pitch, double scale,
                    cudaStream_t st);
 
+// the same along mode 0 of a padded [511][groups][512] tensor (strided tiles),
+// core in the mode-0 lane order (fl_apply_full_lanes)
+int dst_pass_lanes_mode0(const double* x, double* y, const double* core_l, int64_t groups, double scale,
+                         cudaStream_t st);
+
 // y = scale * F x along the middle axis of [outer][n][inner]; with core != nullptr
 // y = scale * F diag(core) F x (core in the layout of x)
 int dst_mode(const double* x, double* y, int64_t outer, int64_t n, int64_t inner, double scale,

@@ -109,11 +109,10 @@ def padded_pitch(n):
     return (n + 15) // 16 * 16
 
 
-def lane_core(core):
-    """The core of an operator with n_last = 511 in the lane order read by
-    the register-resident fused pass (see fl_apply_full_lanes in
-    include/fraclap_b200.h): lines = all but the last mode, padded to a
-    multiple of 16; rows 1-based in [0, 512) with row 0 = 0."""
+def line_lane_core(core):
+    """Lane order of a core over contiguous lines (fl_dst1_core_lanes):
+    lines = all but the last mode (n_last = 511), padded to a multiple of
+    16; rows 1-based in [0, 512) with row 0 = 0."""
     n = core.shape[-1]
     if n != 511:
         raise ValueError("lane order is defined for n_last = 511")
@@ -125,13 +124,29 @@ def lane_core(core):
     return c.reshape(Lp // 4, 2, 2, 16, 32).permute(0, 4, 1, 3, 2).contiguous()
 
 
+def lane_core(core):
+    """The core of an operator with n_0 = n_last = 511 in the mode-0 lane
+    order read by the fused pass of fl_apply_full_lanes (see
+    include/fraclap_b200.h): G padded to [511][n1][512], unit
+    u = (i1 * 32 + c) * 4 + w over columns 16c + 4w + (2f + e), entry
+    [u][i][f][q][e] = G[32q + i - 1][i1][16c + 4w + 2f + e] (row 0 = 0)."""
+    if core.shape[0] != 511 or core.shape[-1] != 511:
+        raise ValueError("mode-0 lane order is defined for n_0 = n_last = 511")
+    g = core.numel() // (511 * 511)
+    c = torch.zeros((512, g, 512), dtype=torch.float64, device=core.device)
+    c[1:, :, :511].copy_(core.reshape(511, g, 511))
+    # r = 32q + i, column = 16c + 4w + 2f + e  ->  [g][c][w][i][f][q][e]
+    c = c.reshape(16, 32, g, 32, 4, 2, 2).permute(2, 3, 4, 1, 5, 0, 6)
+    return c.reshape(g * 128, 32, 2, 16, 2).contiguous()
+
+
 def lane_core_inverse(core_l, dims):
-    """Dense core (dims) from its lane order (inverse of lane_core)."""
-    L = 1
-    for d in dims[:-1]:
-        L *= d
-    c = core_l.permute(0, 2, 4, 3, 1).reshape(-1, 512)
-    return c[:L, 1:].reshape(dims).contiguous()
+    """Dense core (dims) from its mode-0 lane order (inverse of lane_core)."""
+    g = 1
+    for d in dims[1:-1]:
+        g *= d
+    c = core_l.reshape(g, 32, 4, 32, 2, 16, 2).permute(5, 3, 0, 1, 2, 4, 6).reshape(512, g, 512)
+    return c[1:, :, :511].reshape(dims).contiguous()
 
 
 class FullOperator:
@@ -160,10 +175,11 @@ class FullOperator:
         if padded and not can_pad:
             raise ValueError("the padded layout needs sine modes of FFT length")
         self.pitch = padded_pitch(dims[-1]) if padded else None
+        lane_dims = dims[0] == 511 and dims[-1] == 511
         if lanes is None:
-            lanes = bool(padded) and dims[-1] == 511 and os.environ.get("FL_REG", "1") != "0"
-        if lanes and not (padded and dims[-1] == 511):
-            raise ValueError("the lane-ordered core is defined for a padded operator with n_last = 511")
+            lanes = bool(padded) and lane_dims and os.environ.get("FL_REG", "1") != "0"
+        if lanes and not (padded and lane_dims):
+            raise ValueError("the lane-ordered core is defined for a padded operator with n_0 = n_last = 511")
         self.lanes = bool(lanes)
         self.core_p = self.core_l = None
         if padded:
@@ -232,10 +248,25 @@ class FullOperator:
         nl = dims[-1]
         xp, yp, wp = _lib.ptr(x), _lib.ptr(y), _lib.ptr(self.work)
         cp = _lib.ptr(self.core_l if self.lanes else self.core_p)
+        if self.lanes:
+            # fl_apply_full_lanes: last mode contiguous (dense rows -> padded),
+            # mode 1, mode 0 fused with the core, mode 1, last mode back
+            n1 = dims[1] if len(dims) == 3 else 1
+            lines = dims[0] * n1
+            dl, pl = (0, 1, 0, nl), (0, 1, 0, P)
+            mid = (n1 * P, P, 0, 0)
+            out = [("dst_mode2", (xp, wp, None, nl, 1, lines, 1, 1, dl, pl, 1.0))]
+            if len(dims) == 3:
+                out.append(("dst_mode1", (wp, wp, None, n1, 0, dims[0], 1, P, mid, mid, 1.0)))
+            out.append(("dst_core_mode0", ("lanes0", wp, wp, cp, n1, 1.0)))
+            if len(dims) == 3:
+                out.append(("dst_mode1", (wp, wp, None, n1, 0, dims[0], 1, P, mid, mid, 1.0)))
+            out.append(("dst_mode2", (wp, yp, None, nl, 1, lines, 1, 1, pl, dl, self.alpha)))
+            return out
         if len(dims) == 2:
             n0 = dims[0]
             dense, pad, line = (0, nl, 0, 0), (0, P, 0, 0), (0, 1, 0, P)
-            fused = ("lanes", wp, wp, cp, n0, P, 1.0) if self.lanes else (wp, wp, cp, nl, 1, n0, 1, 1, line, line, 1.0)
+            fused = (wp, wp, cp, nl, 1, n0, 1, 1, line, line, 1.0)
             # flag 2 = FL_PASS_PAD_WRITE: the first pass may write the work tensor's padding
             return [("dst_mode0", (xp, wp, None, n0, 2, 1, 1, nl, dense, pad, 1.0)),
                     ("dst_core_mode1", fused),
@@ -243,8 +274,7 @@ class FullOperator:
         n0, n1 = dims[0], dims[1]
         dense0, pad0 = (0, n1 * nl, nl, 0), (0, n1 * P, P, 0)
         mid, line = (n1 * P, P, 0, 0), (0, 1, 0, P)
-        fused = (("lanes", wp, wp, cp, n0 * n1, P, 1.0) if self.lanes
-                 else (wp, wp, cp, nl, 1, n0 * n1, 1, 1, line, line, 1.0))
+        fused = (wp, wp, cp, nl, 1, n0 * n1, 1, 1, line, line, 1.0)
         # flag 2 = FL_PASS_PAD_WRITE: the first pass may write the work tensor's padding
         return [("dst_mode0", (xp, wp, None, n0, 2, 1, n1, nl, dense0, pad0, 1.0)),
                 ("dst_mode1", (wp, wp, None, n1, 0, n0, 1, P, mid, mid, 1.0)),
@@ -259,6 +289,10 @@ def run_pass(args, stream=None):
     if args[0] == "lanes":
         _, x, y, c, lines, pitch, scale = args
         _lib.call("fl_dst1_core_lanes", x, y, c, lines, pitch, float(scale), s)
+        return
+    if args[0] == "lanes0":
+        _, x, y, c, groups, scale = args
+        _lib.call("fl_dst1_core_lanes_mode0", x, y, c, groups, float(scale), s)
         return
     x, y, c, n, contig, outer, groups, width, lin, lout, scale = args
     _lib.call("fl_dst1_pass", x, y, c, n, contig, outer, groups, width, _lib.dims_arr(lin), _lib.dims_arr(lout),

@@ -215,14 +215,14 @@ def test_dst1_core_lanes_matches_oracle(L):
     want = oracle.dst(core * oracle.dst(x, axis=1), axis=1)
     xp = torch.full((L, 512), 3.0, dtype=torch.float64, device="cuda")  # padding column must stay inert
     xp[:, :n] = torch.tensor(x, device="cuda")
-    cl = full.lane_core(torch.tensor(core, device="cuda"))
+    cl = full.line_lane_core(torch.tensor(core, device="cuda"))
     full.run_pass(("lanes", _lib.ptr(xp), _lib.ptr(xp), _lib.ptr(cl), L, 512, 2.0))
     got = xp.cpu().numpy()
     assert rel(got[:, :n], 2.0 * want) <= 1e-13
     assert np.all(got[:, n:] == 3.0)
 
 
-@pytest.mark.parametrize("dims", [(511, 511), (63, 511), (7, 15, 511), (31, 63, 511)])
+@pytest.mark.parametrize("dims", [(511, 511), (511, 7, 511), (511, 63, 511)])
 def test_apply_full_lanes_matches_oracle(dims):
     """fl_apply_full_lanes (register-resident passes, lane-ordered core) vs
     the oracle and vs the padded path with the natural core layout."""

@@ -73,14 +73,13 @@ def test_spectrum_validation_and_ladders():
 
 
 def test_lane_core_order_roundtrip():
-    """The lane order of the n = 511 core (host-side permutation) is a
-    bijection onto the documented entries, with zero padding."""
+    """The lane orders of the n = 511 cores (host-side permutations) are
+    bijections onto the documented entries, with zero padding."""
     import torch
-    from paper_1809_01971_b200.full import lane_core, lane_core_inverse
+    from paper_1809_01971_b200.full import lane_core, lane_core_inverse, line_lane_core
     c = torch.randn(3, 11, 511, dtype=torch.float64)
-    cl = lane_core(c)
+    cl = line_lane_core(c)
     assert cl.shape == (12, 32, 2, 16, 2)  # 33 lines -> 48 (multiple of 16) -> 12 units
-    assert torch.equal(lane_core_inverse(cl, (3, 11, 511)), c)
     flat = cl.reshape(12, 32, 32, 2)
     lines = c.reshape(33, 511)
     for u, i, f, q in [(0, 1, 0, 0), (2, 31, 1, 15), (7, 7, 1, 3)]:
@@ -89,3 +88,18 @@ def test_lane_core_order_roundtrip():
             assert flat[u, i, 16 * f + q, e] == lines[line, row - 1]
     assert torch.all(flat[:, 0, 0, :] == 0)  # row 0
     assert torch.all(flat[9:] == 0)  # padded lines
+    # mode-0 order
+    g = torch.randn(511, 3, 511, dtype=torch.float64)
+    gl = lane_core(g)
+    assert gl.shape == (3 * 128, 32, 2, 16, 2)
+    assert torch.equal(lane_core_inverse(gl, (511, 3, 511)), g)
+    fl = gl.reshape(3 * 128, 32, 32, 2)
+    for i1, cc, w, i, f, q in [(0, 0, 0, 1, 0, 0), (2, 31, 3, 31, 1, 15), (1, 7, 2, 5, 0, 9)]:
+        u = (i1 * 32 + cc) * 4 + w
+        for e in range(2):
+            col, r = 16 * cc + 4 * w + 2 * f + e, 32 * q + i
+            want = g[r - 1, i1, col] if col < 511 else 0.0
+            assert fl[u, i, 16 * f + q, e] == want
+    assert torch.all(fl[:, 0, 0, :] == 0)
+    g2 = torch.randn(511, 511, dtype=torch.float64)
+    assert torch.equal(lane_core_inverse(lane_core(g2), (511, 511)), g2)
