@@ -187,6 +187,47 @@ bool reg_enabled() {
   return v == 1;
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 tma_encoder();
+
+#ifndef FL_REG_TMA
+#define FL_REG_TMA 1
+#endif
+
+// tensor map of a 16-byte aligned strided input (element (o, g, c, j) at
+// o*os + g*gp + c + j*js) with 16-column x 256-row boxes, 128-byte swizzle
+bool reg_tensor_map(const DstArgs& a, CUtensorMap* map) {
+  auto enc = tma_encoder();
+  if (!enc) return false;
+  const uint64_t es = sizeof(double);
+  const uint64_t rows_b = (uint64_t)a.in_js * es;
+  const uint64_t grp_b = a.groups > 1 ? (uint64_t)a.in_gp * es : rows_b * (uint64_t)a.n;
+  const uint64_t out_b = a.outer > 1 ? (uint64_t)a.in_os * es : grp_b * (uint64_t)a.groups;
+  if (rows_b % 16 || grp_b % 16 || out_b % 16) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)a.wv, (cuuint64_t)a.n, (cuuint64_t)a.groups, (cuuint64_t)a.outer};
+  cuuint64_t strides[3] = {rows_b, grp_b, out_b};
+  cuuint32_t box[4] = {16, 256, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(a.x), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int SIN, int SOUT, bool MID, bool TMA>
+int launch_reg_k(const DstArgs& a, const CUtensorMap& map, cudaStream_t st) {
+  auto kern = rg::k_dst_grp<SIN, SOUT, MID, TMA>;
+  constexpr size_t SMEM = rg::grp_smem_bytes();
+  static bool attr = false;
+  if (!attr) {
+    FL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    attr = true;
+  }
+  const int64_t cap = 2 * (int64_t)sm_count();
+  const int grid = (int)(a.ntiles < cap ? a.ntiles : cap);
+  kern<<<grid, 32 * rg::NWARP, SMEM, st>>>(a, map);
+  FL_LAUNCH_CHECK();
+  return FL_OK;
+}
+
 template <int SIN, int SOUT, bool MID>
 int launch_reg(DstArgs a, cudaStream_t st) {
   if (SIN == rg::SIDE_CONTIG) {
@@ -202,18 +243,16 @@ int launch_reg(DstArgs a, cudaStream_t st) {
     a.div_blk = make_fastdiv((uint32_t)(a.groups * a.nchunks));
     a.div_chunk = make_fastdiv((uint32_t)a.nchunks);
   }
-  auto kern = rg::k_dst_grp<SIN, SOUT, MID>;
-  constexpr size_t SMEM = rg::grp_smem_bytes();
-  static bool attr = false;
-  if (!attr) {
-    FL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
-    attr = true;
+  CUtensorMap map{};
+  if constexpr (SIN == rg::SIDE_VEC) {
+    static int use = -1;
+    if (use < 0) {
+      const char* e = getenv("FL_REG_TMA");
+      use = e ? (e[0] != '0') : FL_REG_TMA;
+    }
+    if (use && reg_tensor_map(a, &map)) return launch_reg_k<SIN, SOUT, MID, true>(a, map, st);
   }
-  const int64_t cap = 2 * (int64_t)sm_count();
-  const int grid = (int)(a.ntiles < cap ? a.ntiles : cap);
-  kern<<<grid, 32 * rg::NWARP, SMEM, st>>>(a);
-  FL_LAUNCH_CHECK();
-  return FL_OK;
+  return launch_reg_k<SIN, SOUT, MID, false>(a, map, st);
 }
 
 // ---- TMA-fed strided pass (dst_tma.cuh) ----------------------------------

@@ -30,6 +30,7 @@
 #include <type_traits>
 
 #include "dst_fft.cuh"
+#include "dst_tma.cuh"
 
 namespace fl {
 namespace rg {
@@ -643,23 +644,59 @@ __device__ __forceinline__ void store_contig(const DstArgs& a, uint32_t t, doubl
 // Strided passes (SIDE_IN != SIDE_CONTIG): CTA-cooperative loads and stores.
 // Contiguous fused pass (MID): warp-local loads, core from the lane-ordered
 // core layout (fl_core_lanes), z through the warp's part of the tile.
-template <int SIDE_IN, int SIDE_OUT, bool MID>
-__global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a) {
+// TMA load of strided tile t: two 256-row boxes of 16 columns, rows -1 ..
+// 254 (row -1 out of range: zeros) and 255 .. 510 into tile rows 0 .. 511;
+// the 128-byte swizzle is exactly tidx's chunk ^ (row & 7)
+__device__ __forceinline__ void tma_issue_grp(const DstArgs& a, const CUtensorMap* map, uint32_t t, double2* tile,
+                                              uint64_t* bar) {
+  const uint32_t o = a.div_blk.div(t);
+  const uint32_t r = t - o * a.div_blk.d;
+  const uint32_t g = a.div_chunk.div(r);
+  const int c0 = (int)(r - g * a.div_chunk.d) * 16;
+  mbar_expect_tx(bar, (uint32_t)(TILE * sizeof(double2)));
+  tma_load_4d(tile, map, c0, -1, (int)g, (int)o, bar);
+  tma_load_4d(tile + TILE / 2, map, c0, 255, (int)g, (int)o, bar);
+}
+
+template <int SIDE_IN, int SIDE_OUT, bool MID, bool TMA>
+__global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, const __grid_constant__ CUtensorMap map) {
   extern __shared__ __align__(1024) double2 smem_grp[];
   double2* const tile = smem_grp;
   double2* const scr_all = smem_grp + TILE;
+  uint64_t* const bar = reinterpret_cast<uint64_t*>(scr_all + NWARP * SCR);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* const scr = scr_all + SCR * w;
   const uint32_t stile = smem_u32(tile);
   const uint32_t ntiles = (uint32_t)a.ntiles;
   uint32_t t = blockIdx.x;
   constexpr bool STRIDED = SIDE_IN != SIDE_CONTIG;
-  if (t < ntiles) {
-    if (STRIDED) issue_strided<SIDE_IN>(a, t, stile, w, lane); else issue_contig(a, t, stile, w, lane);
+  static_assert(!TMA || SIDE_IN == SIDE_VEC, "TMA tiles need 16-byte aligned strided input");
+  uint32_t phase = 0;
+  auto issue_next = [&](uint32_t tt) {
+    if constexpr (TMA) {
+      if (threadIdx.x == 0 && !(FL_REG_NOMEM == 1 || FL_REG_NOMEM == 2)) tma_issue_grp(a, &map, tt, tile, bar);
+    } else if constexpr (STRIDED) {
+      issue_strided<SIDE_IN>(a, tt, stile, w, lane);
+    } else {
+      issue_contig(a, tt, stile, w, lane);
+    }
+  };
+  if constexpr (TMA) {
+    if ((stile & 1023u) != 0) __trap();  // the 128-byte swizzle needs a 1024-byte aligned tile
+    if (threadIdx.x == 0) {
+      mbar_init(bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
   }
+  if (t < ntiles) issue_next(t);
   cp_commit();
   for (; t < ntiles; t += gridDim.x) {
     const uint32_t tn = t + gridDim.x;
+    if constexpr (TMA) {
+      if (!(FL_REG_NOMEM == 1 || FL_REG_NOMEM == 2)) mbar_wait(bar, phase);
+      phase ^= 1;
+    }
     cp_wait<0>();
     if (STRIDED) __syncthreads(); else __syncwarp();
     double2 v[32], ev[16], od[16];
@@ -673,9 +710,7 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a) {
       const Lane c = lane_consts(a, lane);
       pre_read<STRIDED ? RAW_STRIDED : RAW_CONTIG>(tile, w, c, v, sha, shb);
       if (STRIDED) __syncthreads(); else __syncwarp();
-      if (tn < ntiles) {
-        if (STRIDED) issue_strided<SIDE_IN>(a, tn, stile, w, lane); else issue_contig(a, tn, stile, w, lane);
-      }
+      if (tn < ntiles) issue_next(tn);
       cp_commit();
       fft_split(scr, c, v, ev, od);
     } else {
@@ -691,7 +726,9 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a) {
           pre_read<RAW_Z>(tile, w, lane_consts<true>(a, lane), v);
         }
         // phase 0: the tile is consumed, quarter w (16 KB) is the warp's own
-        // from here; phase 1: every warp has read its z, the tile is free
+        // from here; phase 1: every warp has read its z, the tile is free (z
+        // was written through the generic proxy: fence before TMA refills it)
+        if (TMA && ph == 1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         if (STRIDED) __syncthreads(); else __syncwarp();
         if (ph == 0) {
           // bring the unit's lane-ordered core slice into quarter w while the
@@ -706,9 +743,7 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a) {
           }
           cp_commit();
         } else {
-          if (tn < ntiles) {
-            if (STRIDED) issue_strided<SIDE_IN>(a, tn, stile, w, lane); else issue_contig(a, tn, stile, w, lane);
-          }
+          if (tn < ntiles) issue_next(tn);
           cp_commit();
         }
         // shared addressing survives: the laundered part is an integer offset
@@ -752,7 +787,7 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a) {
   cp_wait<0>();
 }
 
-constexpr size_t grp_smem_bytes() { return (size_t)(TILE + NWARP * SCR) * sizeof(double2); }
+constexpr size_t grp_smem_bytes() { return (size_t)(TILE + NWARP * SCR) * sizeof(double2) + 16; }
 
 }  // namespace rg
 }  // namespace fl
