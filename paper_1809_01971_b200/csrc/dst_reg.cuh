@@ -329,21 +329,24 @@ __device__ __forceinline__ Lane lane_consts(const DstArgs& a, int lane_in) {
   return c;
 }
 
-// DST-I pre-processing of rows j and N - j into y_j (m = row block, j = q + 16 m)
-__device__ __forceinline__ double2 pre_y(const Lane& c, int m, double2 xa, double2 xb) {
+// DST-I pre-processing of rows j and N - j into sc * y_j (m = row block,
+// j = q + 16 m): the pass's output scale rides on the coefficients
+// (s + 1/2) sc and (s - 1/2) sc, free next to the s +- 1/2 it replaces
+__device__ __forceinline__ double2 pre_y(const Lane& c, int m, double2 xa, double2 xb, double sc, double hsc) {
   const double s = fma(c.sq, kc(m), c.cq * ks(m));  // sin(pi (q + 16 m) / 512)
-  const double sp = s + 0.5, sm = s - 0.5;
+  const double sp = fma(s, sc, hsc), sm = fma(s, sc, -hsc);
   double2 y = make_double2(fma(sp, xa.x, sm * xb.x), fma(sp, xa.y, sm * xb.y));
   if (m == 0 && c.q == 0) y = make_double2(0.0, 0.0);
-  if (m == 16 && c.q == 0) y = make_double2(2.0 * xa.x, 2.0 * xa.y);
+  if (m == 16 && c.q == 0) y = make_double2((sc + sc) * xa.x, (sc + sc) * xa.y);
   return y;
 }
 
 // pre-processed input y_{q + 16 m} of FFT f of warp w
 template <int RAW>
-__device__ __forceinline__ void pre_read(const double2* tile, int w, const Lane& c_in, double2 (&v)[32], int sha = 0,
-                                         int shb = 0) {
+__device__ __forceinline__ void pre_read(const double2* tile, int w, const Lane& c_in, double2 (&v)[32], double sc,
+                                         int sha = 0, int shb = 0) {
   Lane c = c_in;
+  const double hsc = 0.5 * sc;
   const int f = c.f, q = c.q, q7 = q & 7;
   // each batch's sines are computed from freshly laundered sin/cos, so the
   // compiler cannot precompute all 32 of them ahead of the loads
@@ -367,7 +370,7 @@ __device__ __forceinline__ void pre_read(const double2* tile, int w, const Lane&
       const int j = (m == 0) ? (q == 0 ? 1 : q) : q + 16 * m;  // q + 16 m (row 0 -> any valid row)
       const int jp = 512 - q - 16 * m;                         // N - j (m = 0, q = 0: 512 -> clamp)
       const int jb = (m == 0 && q == 0) ? 1 : jp;
-      v[m] = pre_y(c, m, make_double2(ra[j], rb[j]), make_double2(ra[jb], rb[jb]));
+      v[m] = pre_y(c, m, make_double2(ra[j], rb[j]), make_double2(ra[jb], rb[jb]), sc, hsc);
     }
   } else if constexpr (RAW == RAW_STRIDED) {
     const int ch = 2 * w + f;
@@ -378,7 +381,7 @@ __device__ __forceinline__ void pre_read(const double2* tile, int w, const Lane&
       batch(m);
       const int ia = la + 128 * m;
       const int ib = (m == 0 && q == 0) ? la : lb + 128 * (31 - m);
-      v[m] = pre_y(c, m, tile[ia], tile[ib]);
+      v[m] = pre_y(c, m, tile[ia], tile[ib], sc, hsc);
     }
   } else {
     // z layout in warp w's 16 KB of the tile
@@ -393,7 +396,7 @@ __device__ __forceinline__ void pre_read(const double2* tile, int w, const Lane&
       const int ia = (la ^ ((m >> 1) & 7)) + 32 * m;
       int ib = q == 0 ? ((lb ^ (((32 - m) >> 1) & 7)) + 32 * (31 - m)) : ((lb ^ (((31 - m) >> 1) & 7)) + 32 * (31 - m));
       if (m == 0 && q == 0) ib = ia;
-      v[m] = pre_y(c, m, zt[ia], zt[ib]);
+      v[m] = pre_y(c, m, zt[ia], zt[ib], sc, hsc);
     }
   }
 }
@@ -708,7 +711,7 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
     }
     if constexpr (!MID) {
       const Lane c = lane_consts(a, lane);
-      pre_read<STRIDED ? RAW_STRIDED : RAW_CONTIG>(tile, w, c, v, sha, shb);
+      pre_read<STRIDED ? RAW_STRIDED : RAW_CONTIG>(tile, w, c, v, 0.5 * a.scale, sha, shb);
       if (STRIDED) __syncthreads(); else __syncwarp();
       if (tn < ntiles) issue_next(tn);
       cp_commit();
@@ -721,9 +724,10 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
         // v is (re)defined at the top of both phases, so it is dead across
         // the back edge
         if (ph == 0) {
-          pre_read<STRIDED ? RAW_STRIDED : RAW_CONTIG>(tile, w, lane_consts<true>(a, lane), v, sha, shb);
+          pre_read<STRIDED ? RAW_STRIDED : RAW_CONTIG>(tile, w, lane_consts<true>(a, lane), v, 0.25 * a.scale, sha,
+                                                       shb);
         } else {
-          pre_read<RAW_Z>(tile, w, lane_consts<true>(a, lane), v);
+          pre_read<RAW_Z>(tile, w, lane_consts<true>(a, lane), v, 1.0);
         }
         // phase 0: the tile is consumed, quarter w (16 KB) is the warp's own
         // from here; phase 1: every warp has read its z, the tile is free (z
@@ -773,7 +777,8 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
         }
       }
     }
-    const double sc = (MID ? 0.25 : 0.5) * a.scale;
+    // the scale (0.5 per split, nrm, alpha) was applied in the first pre-processing
+    const double sc = 1.0;
     if constexpr (STRIDED) {
       if (FL_REG_DIRECT_STORE) {
         store_strided_direct<SIDE_OUT>(a, t, w, lane >> 4, lane & 15, ev, od, sc);

@@ -39,11 +39,11 @@ def t(fn, reps=20):
 
 B = 16 * n ** 3 / 1e9
 out = {"FL_REG": os.environ.get("FL_REG", "0")}
-for name, a in op.passes(x, y):
+for k, (name, a) in enumerate(op.passes(x, y)):
     ms = t(lambda: full.run_pass(a))
     fac = 1.5 if "core" in name else 1.0
-    out[name] = "%.3f ms (%.0f GB/s)" % (ms, fac * B / ms * 1e3)
-ms = t(lambda: op(x, out=y))
+    out["%d:%s" % (k, name)] = "%.3f ms (%.0f GB/s)" % (ms, fac * B / ms * 1e3)
+ms = t(lambda: op(x, out=y), reps=50)
 out["apply"] = "%.3f ms (%.1f GDoF/s)" % (ms, n ** 3 / ms / 1e6)
 print(out, flush=True)
 if check:
