@@ -212,9 +212,31 @@ bool reg_tensor_map(const DstArgs& a, CUtensorMap* map) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int SIN, int SOUT, bool MID, bool TMA>
-int launch_reg_k(const DstArgs& a, const CUtensorMap& map, cudaStream_t st) {
-  auto kern = rg::k_dst_grp<SIN, SOUT, MID, TMA>;
+// the three output maps of the TMA-store phase (dst_reg.cuh, OutMaps)
+bool reg_out_maps(const DstArgs& a, rg::OutMaps* m) {
+  auto enc = tma_encoder();
+  if (!enc) return false;
+  const uint64_t es = sizeof(double);
+  const uint64_t row_b = (uint64_t)a.out_js * es;
+  const uint64_t grp_b = a.groups > 1 ? (uint64_t)a.out_gp * es : row_b * 512;
+  const uint64_t out_b = a.outer > 1 ? (uint64_t)a.out_os * es : grp_b * (uint64_t)a.groups;
+  if (row_b % 16 || grp_b % 16 || out_b % 16) return false;
+  cuuint64_t dims[5] = {(cuuint64_t)a.wv, 16, 32, (cuuint64_t)a.groups, (cuuint64_t)a.outer};
+  cuuint64_t strides[4] = {32 * row_b, row_b, grp_b, out_b};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  const cuuint32_t boxes[3][5] = {{16, 8, 32, 1, 1}, {16, 7, 32, 1, 1}, {16, 1, 31, 1, 1}};
+  CUtensorMap* maps[3] = {&m->a, &m->b, &m->c};
+  for (int k = 0; k < 3; ++k)
+    if (enc(maps[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, a.y, dims, strides, const_cast<cuuint32_t*>(boxes[k]), estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  return true;
+}
+
+template <int SIN, int SOUT, bool MID, bool TMA, bool TST>
+int launch_reg_k(const DstArgs& a, const CUtensorMap& map, const rg::OutMaps& om, cudaStream_t st) {
+  auto kern = rg::k_dst_grp<SIN, SOUT, MID, TMA, TST>;
   constexpr size_t SMEM = rg::grp_smem_bytes();
   static bool attr = false;
   if (!attr) {
@@ -223,9 +245,27 @@ int launch_reg_k(const DstArgs& a, const CUtensorMap& map, cudaStream_t st) {
   }
   const int64_t cap = 2 * (int64_t)sm_count();
   const int grid = (int)(a.ntiles < cap ? a.ntiles : cap);
-  kern<<<grid, 32 * rg::NWARP, SMEM, st>>>(a, map);
+  kern<<<grid, 32 * rg::NWARP, SMEM, st>>>(a, map, om);
   FL_LAUNCH_CHECK();
   return FL_OK;
+}
+
+#ifndef FL_REG_TST
+#define FL_REG_TST 1
+#endif
+
+template <int SIN, int SOUT, bool MID, bool TMA>
+int launch_reg_o(const DstArgs& a, const CUtensorMap& map, cudaStream_t st) {
+  rg::OutMaps om{};
+  if constexpr (SOUT == rg::SIDE_VEC) {
+    static int use = -1;
+    if (use < 0) {
+      const char* e = getenv("FL_REG_TST");
+      use = e ? (e[0] != '0') : FL_REG_TST;
+    }
+    if (use && a.n == 511 && reg_out_maps(a, &om)) return launch_reg_k<SIN, SOUT, MID, TMA, true>(a, map, om, st);
+  }
+  return launch_reg_k<SIN, SOUT, MID, TMA, false>(a, map, om, st);
 }
 
 template <int SIN, int SOUT, bool MID>
@@ -250,9 +290,9 @@ int launch_reg(DstArgs a, cudaStream_t st) {
       const char* e = getenv("FL_REG_TMA");
       use = e ? (e[0] != '0') : FL_REG_TMA;
     }
-    if (use && reg_tensor_map(a, &map)) return launch_reg_k<SIN, SOUT, MID, true>(a, map, st);
+    if (use && reg_tensor_map(a, &map)) return launch_reg_o<SIN, SOUT, MID, true>(a, map, st);
   }
-  return launch_reg_k<SIN, SOUT, MID, false>(a, map, st);
+  return launch_reg_o<SIN, SOUT, MID, false>(a, map, st);
 }
 
 // ---- TMA-fed strided pass (dst_tma.cuh) ----------------------------------

@@ -643,6 +643,79 @@ __device__ __forceinline__ void store_contig(const DstArgs& a, uint32_t t, doubl
   }
 }
 
+// ---- TMA tensor stores of strided outputs ---------------------------------
+// Lane q holds rows 32q .. 32q+31, i.e. global rows g = r - 1 = 32 qq + ii
+// with (qq, ii) = (q, j - 1) for j = r - 32q >= 1 and (q - 1, 31) for j = 0.
+// Staged as [ii][qq][16 columns] (the box of a 5-D tensor map {columns, qq
+// (stride 32 rows), ii (stride 1 row), groups, outer}), rows written together
+// (same ii, 8 consecutive qq) fall in 8 bank groups under the 128-byte
+// swizzle.  Row 511 does not exist, so half 1 is two boxes: qq 8..14 x 32
+// and qq 15 x 31 (three maps: A = qq 0..7, B, C).
+struct OutMaps {
+  CUtensorMap a, b, c;
+};
+
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3,
+                                             int c4) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// double2 index of (qq, ii, chunk) in the staging of half hh
+__device__ __forceinline__ int stg_tma_idx(int hh, int qq, int ii, int ch) {
+  if (hh == 0) {
+    const int R = ii * 8 + qq;
+    return R * 8 + (ch ^ (R & 7));
+  }
+  if (qq < 15) {
+    const int R = ii * 7 + (qq - 8);
+    return R * 8 + (ch ^ (R & 7));
+  }
+  return 1792 + ii * 8 + (ch ^ (ii & 7));
+}
+
+__device__ __forceinline__ void store_strided_tma(const DstArgs& a, const OutMaps* maps, uint32_t t, double2* stg,
+                                                  int w, int f, int q, const double2 (&ev)[16],
+                                                  const double2 (&od)[16]) {
+  const int ch = 2 * w + f;
+  const uint32_t o = a.div_blk.div(t);
+  const uint32_t rr = t - o * a.div_blk.d;
+  const uint32_t g = a.div_chunk.div(rr);
+  const int c0 = (int)(rr - g * a.div_chunk.d) * 16;
+  // the staging interleaves all four warps' columns over the whole 32 KB of
+  // scratch: every warp must be done with its exchange/spectrum first
+  __syncthreads();
+#pragma unroll 1
+  for (int hh = 0; hh < 2; ++hh) {
+    if ((q >> 3) == hh) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i > 0) stg[stg_tma_idx(hh, q, 2 * i - 1, ch)] = ev[i];  // j = 2i
+        stg[stg_tma_idx(hh, q, 2 * i, ch)] = od[i];                 // j = 2i + 1
+      }
+    }
+    if (q >= 1 && ((q - 1) >> 3) == hh) stg[stg_tma_idx(hh, q - 1, 31, ch)] = ev[0];  // j = 0
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0 && !(FL_REG_NOMEM == 1 || FL_REG_NOMEM == 3)) {
+      if (hh == 0) {
+        tma_store_5d(&maps->a, stg, c0, 0, 0, (int)g, (int)o);
+      } else {
+        tma_store_5d(&maps->b, stg, c0, 8, 0, (int)g, (int)o);
+        tma_store_5d(&maps->c, stg + 1792, c0, 15, 0, (int)g, (int)o);
+      }
+      bulk_commit();
+      bulk_wait_read();
+    }
+    __syncthreads();
+  }
+}
+
 // Persistent CTAs of 4 warps (one 16-line tile at a time), 2 per SM.
 // Strided passes (SIDE_IN != SIDE_CONTIG): CTA-cooperative loads and stores.
 // Contiguous fused pass (MID): warp-local loads, core from the lane-ordered
@@ -661,8 +734,9 @@ __device__ __forceinline__ void tma_issue_grp(const DstArgs& a, const CUtensorMa
   tma_load_4d(tile + TILE / 2, map, c0, 255, (int)g, (int)o, bar);
 }
 
-template <int SIDE_IN, int SIDE_OUT, bool MID, bool TMA>
-__global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, const __grid_constant__ CUtensorMap map) {
+template <int SIDE_IN, int SIDE_OUT, bool MID, bool TMA, bool TST>
+__global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, const __grid_constant__ CUtensorMap map,
+                                                           const __grid_constant__ OutMaps omaps) {
   extern __shared__ __align__(1024) double2 smem_grp[];
   double2* const tile = smem_grp;
   double2* const scr_all = smem_grp + TILE;
@@ -674,6 +748,7 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
   uint32_t t = blockIdx.x;
   constexpr bool STRIDED = SIDE_IN != SIDE_CONTIG;
   static_assert(!TMA || SIDE_IN == SIDE_VEC, "TMA tiles need 16-byte aligned strided input");
+  static_assert(!TST || SIDE_OUT == SIDE_VEC, "TMA stores need 16-byte aligned strided output");
   uint32_t phase = 0;
   auto issue_next = [&](uint32_t tt) {
     if constexpr (TMA) {
@@ -780,7 +855,9 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
     // the scale (0.5 per split, nrm, alpha) was applied in the first pre-processing
     const double sc = 1.0;
     if constexpr (STRIDED) {
-      if (FL_REG_DIRECT_STORE) {
+      if constexpr (TST) {
+        store_strided_tma(a, &omaps, t, scr_all, w, lane >> 4, lane & 15, ev, od);
+      } else if (FL_REG_DIRECT_STORE) {
         store_strided_direct<SIDE_OUT>(a, t, w, lane >> 4, lane & 15, ev, od, sc);
       } else {
         store_strided<SIDE_OUT>(a, t, scr_all, w, lane, lane >> 4, lane & 15, ev, od, sc);
@@ -790,6 +867,7 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
     }
   }
   cp_wait<0>();
+  if (TST && threadIdx.x == 0) bulk_wait_all();
 }
 
 constexpr size_t grp_smem_bytes() { return (size_t)(TILE + NWARP * SCR) * sizeof(double2) + 16; }

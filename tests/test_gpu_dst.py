@@ -243,3 +243,19 @@ def test_apply_full_lanes_matches_oracle(dims):
     for _, a in op.passes(xt, z):
         full.run_pass(a)
     assert rel(z.cpu().numpy(), want) <= 1e-12
+
+
+@pytest.mark.parametrize("blocks,inplace", [(40, True), (37, False)])
+def test_dst1_pass_n511_many_tiles_per_cta(blocks, inplace):
+    """n = 511 strided passes with more tiles than resident CTAs (TMA loads,
+    TMA tensor stores through the CTA-wide staging, in place and not)."""
+    from paper_1809_01971_b200 import _lib
+    n, P = 511, 512
+    g = torch.Generator(device="cuda")
+    g.manual_seed(blocks)
+    x = torch.randn((blocks, n, P), dtype=torch.float64, device="cuda", generator=g)
+    want = oracle.dst(x.cpu().numpy(), axis=1)
+    y = x if inplace else torch.full_like(x, 7.0)
+    lay = (n * P, P, 0, 0)
+    full.run_pass((_lib.ptr(x), _lib.ptr(y), None, n, 0, blocks, 1, P, lay, lay, 1.0))
+    assert rel(y.cpu().numpy(), want) <= 1e-13
