@@ -596,45 +596,62 @@ __device__ __forceinline__ void store_strided(const DstArgs& a, uint32_t t, doub
   }
 }
 
-// contiguous output of warp w (lines 4w .. 4w+3 of the tile), half hh: rows
-// r in [256 hh, 256 hh + 256) at staging position p = r - 256 hh of line l,
-// word l * 256 + (p ^ (((p >> 5) & 7) << 1 | (l >> 1))), then 256-byte
-// coalesced stores per instruction
+// contiguous output of warp w (lines 4w .. 4w+3 of the tile) through its
+// 8 KB scratch in two halves of positions p = r - 1: [0, 256) (rows 1 .. 256)
+// and [256, 512) (rows 257 .. 511, position 511 is never stored).  Staging
+// [line][256] with 16-byte chunks (positions 2c, 2c+1) at c ^ ((c >> 4) & 7):
+// a lane writes (odd row, next even row) = (od[i], ev[i+1]) as one 16-byte
+// store (8 active lanes of a quarter warp hit 8 chunk columns), the read-back
+// is one 16-byte load per lane, 512 contiguous bytes per warp instruction,
+// stored as 16 bytes where the line is 16-byte aligned.
+__device__ __forceinline__ int cstg(int p) { return (((p >> 1) ^ ((p >> 5) & 7)) << 1) | (p & 1); }
+
 __device__ __forceinline__ void store_contig(const DstArgs& a, uint32_t t, double2* scr, int w, int lane, int f,
                                              int q, const double2 (&ev)[16], const double2 (&od)[16], double sc) {
   const Tile tl = tile_of<SIDE_CONTIG, true>(a, t);
   double* sd = reinterpret_cast<double*>(scr);
+  double* la = sd + (2 * f) * 256;  // line 2f (.x), line 2f + 1 (.y) at + 256
 #pragma unroll 1
   for (int hh = 0; hh < 2; ++hh) {
     if ((q >> 3) == hh) {
-      const int q7 = q & 7;
-      // rows 32 q + 2 i (+1): p = 32 q7 + 2 i (+1); key = q7 << 1 | f (line 2f or 2f+1 has l >> 1 = f)
-      double* b0 = sd + (2 * f) * 256 + 32 * q7;
-      double* b1 = b0 + 256;
-      const int key = (q7 << 1) | f;
+      // rows 32q + 2i + 1 and 32q + 2i + 2: positions pl = 32 (q - 8hh) + 2i (+1)
+      const int base = 32 * (q - 8 * hh);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int pe = (2 * i) ^ key, po = (2 * i + 1) ^ key;
-        if (i > 0 || q > 0) {
-          b0[pe] = sc * ev[i].x;
-          b1[pe] = sc * ev[i].y;
-        }
-        b0[po] = sc * od[i].x;
-        b1[po] = sc * od[i].y;
+      for (int i = 0; i < 15; ++i) {
+        const int pl = base + 2 * i;
+        const int ph = cstg(pl);  // even
+        *reinterpret_cast<double2*>(la + ph) = make_double2(sc * od[i].x, sc * ev[i + 1].x);
+        *reinterpret_cast<double2*>(la + 256 + ph) = make_double2(sc * od[i].y, sc * ev[i + 1].y);
       }
+      const int pl = base + 30;  // row 32q + 31 (od[15]); position + 1 belongs to the next lane
+      la[cstg(pl)] = sc * od[15].x;
+      la[256 + cstg(pl)] = sc * od[15].y;
+    }
+    // row 32q (ev[0], position 32q - 1) of lanes q in [8hh + 1, 8hh + 8]
+    if (q >= 1 && ((q - 1) >> 3) == hh) {
+      const int pl = 32 * q - 1 - 256 * hh;
+      la[cstg(pl)] = sc * ev[0].x;
+      la[256 + cstg(pl)] = sc * ev[0].y;
     }
     __syncwarp();
     if (!(FL_REG_NOMEM == 1 || FL_REG_NOMEM == 3) || a.scale == 12345.0) {
 #pragma unroll
       for (int l = 0; l < 4; ++l) {
         if (4 * w + l < tl.lmax) {
-          double* y = a.y + tl.base + (int64_t)(4 * w + l) * tl.LS + 256 * hh - 1 + lane;  // row r at r - 1
-          const double* src = sd + l * 256;
+          const int64_t off = tl.base + (int64_t)(4 * w + l) * tl.LS + 256 * hh;  // element of position 256 hh
+          const bool al = ((off & 1) == 0) && ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0);
+          double* y = a.y + off;
 #pragma unroll
-          for (int s = 0; s < 8; ++s) {
-            // p = lane + 32 s: the key of p is a per-instruction constant
-            const double val = src[(lane + 32 * s) ^ ((s << 1) | (l >> 1))];
-            if (s > 0 || hh > 0 || lane > 0) y[32 * s] = val;
+          for (int s = 0; s < 4; ++s) {
+            const int c = lane + 32 * s;  // chunk: positions 2c, 2c + 1 of the half
+            const double2 val = *reinterpret_cast<const double2*>(sd + l * 256 + 2 * (c ^ ((c >> 4) & 7)));
+            const bool last = (hh == 1 && c == 127);  // position 511 does not exist
+            if (al && !last) {
+              *reinterpret_cast<double2*>(y + 2 * c) = val;
+            } else {
+              y[2 * c] = val.x;
+              if (!last) y[2 * c + 1] = val.y;
+            }
           }
         }
       }
