@@ -12,19 +12,27 @@
 //     and scans its 16 Re Y values in registers (cross-lane offsets by 4
 //     shuffles).  No CTA barrier inside the FFT.
 //   * global traffic is organised per CTA of 4 warps = 16 lines: on strided
-//     layouts every load/store instruction covers whole 128-byte row
-//     segments (a warp's own 4 columns are only 32 bytes of a row; 32-byte
-//     accesses cost 1.8-2.5x the DRAM bytes and stall the LSU).  The CTA's
-//     tile (64 KB, rows of 16 columns, 16-byte chunks XOR-swizzled by row)
-//     is loaded with cp.async; the next tile's loads are issued as soon as
-//     the current one has been read into registers, so they fly during the
-//     FFTs.  Outputs go through the warps' 8 KB scratch in two halves and
-//     leave as full row segments.
+//     layouts every access covers whole 128-byte row segments (a warp's own
+//     4 columns are only 32 bytes of a row; 32-byte accesses cost 1.8-2.5x
+//     the DRAM bytes and stall the LSU).  Strided tiles (64 KB, rows of 16
+//     columns, 16-byte chunks XOR-swizzled by row = the TMA 128-byte
+//     pattern) arrive by two TMA boxes on an mbarrier (cp.async where the
+//     side is not 16-byte aligned); the next tile is requested as soon as
+//     the current one has been read into registers, so it lands during the
+//     FFTs.  Strided outputs leave by TMA tensor stores from a staging in
+//     the warps' scratch (a 5-D box that makes the staging conflict-free,
+//     see store_strided_tma); contiguous lines by warp-local cp.async loads
+//     and 16-byte staged stores.
+//   * the fused pass (forward, core, inverse) brings the unit's lane-ordered
+//     core slice into the warp's quarter of the consumed tile during the
+//     forward FFT and runs the inverse from z written over it.
 //   * 96 KB of shared memory per CTA, 2 CTAs per SM, up to 255 registers.
 // Every shared-memory and global access is a per-lane base plus a
-// compile-time offset; sines and twiddles come from per-lane constants.
-// Compute-only (no global traffic) the plain pass runs in 0.30 ms at n = 511,
-// the CTA kernel of dst_fft.cuh in 0.47 ms.
+// compile-time offset; sines and twiddles come from per-lane constants, the
+// pass's output scale rides on the pre-processing coefficients.
+// Compute-only (no global traffic) the plain pass runs in 0.32 ms at n = 511
+// (the CTA kernel of dst_fft.cuh: 0.47 ms); with traffic 0.40 ms strided,
+// 0.44 ms contiguous, 0.82 ms fused.
 #pragma once
 
 #include <type_traits>
@@ -733,10 +741,6 @@ __device__ __forceinline__ void store_strided_tma(const DstArgs& a, const OutMap
   }
 }
 
-// Persistent CTAs of 4 warps (one 16-line tile at a time), 2 per SM.
-// Strided passes (SIDE_IN != SIDE_CONTIG): CTA-cooperative loads and stores.
-// Contiguous fused pass (MID): warp-local loads, core from the lane-ordered
-// core layout (fl_core_lanes), z through the warp's part of the tile.
 // TMA load of strided tile t: two 256-row boxes of 16 columns, rows -1 ..
 // 254 (row -1 out of range: zeros) and 255 .. 510 into tile rows 0 .. 511;
 // the 128-byte swizzle is exactly tidx's chunk ^ (row & 7)
@@ -751,6 +755,10 @@ __device__ __forceinline__ void tma_issue_grp(const DstArgs& a, const CUtensorMa
   tma_load_4d(tile + TILE / 2, map, c0, 255, (int)g, (int)o, bar);
 }
 
+// Persistent CTAs of 4 warps (one 16-line tile at a time), 2 per SM.
+// Strided sides: CTA-cooperative tiles (TMA: TMA loads; TST: TMA stores);
+// contiguous sides: warp-local lines.  MID: forward, core (lane-ordered,
+// full.lane_core / line_lane_core), inverse in one pass.
 template <int SIDE_IN, int SIDE_OUT, bool MID, bool TMA, bool TST>
 __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, const __grid_constant__ CUtensorMap map,
                                                            const __grid_constant__ OutMaps omaps) {
