@@ -279,6 +279,36 @@ __device__ __forceinline__ void issue_contig(const DstArgs& a, uint32_t t, uint3
   });
 }
 
+// A warp's 4 lines as one bulk copy when they are one contiguous,
+// 16-byte aligned blob: pitch 512 (padded, 16 KB) or the dense pitch 511
+// (16352 B; the blob starts at line 16t + 4w, an even line, so at a 16-byte
+// aligned offset).  The ragged last tile keeps cp.async (zero fill).
+__device__ __forceinline__ bool contig_bulk(const DstArgs& a, const Tile& tl, int w) {
+  return (tl.LS == 511 || tl.LS == 512) && 4 * w + 3 < tl.lmax && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// contiguous tile issue: bulk copy (lane 0, completes on wbar) or cp.async
+__device__ __forceinline__ void issue_contig_any(const DstArgs& a, uint32_t t, double2* tile, uint32_t stile, int w,
+                                                 int lane, uint64_t* wbar) {
+  const Tile tl = tile_of<SIDE_CONTIG, false>(a, t);
+  if (contig_bulk(a, tl, w)) {
+    if (lane == 0 && !(FL_REG_NOMEM == 1 || FL_REG_NOMEM == 2)) {
+      const uint32_t bytes = (uint32_t)(4 * tl.LS * sizeof(double));
+      mbar_expect_tx(wbar, bytes);
+      bulk_load(tile + 1024 * w, a.x + tl.base + (int64_t)(4 * w) * tl.LS, bytes, wbar);
+    }
+  } else {
+    issue_contig(a, t, stile, w, lane);
+  }
+}
+
 struct Lane {
   int f, q;
   double sq, cq;             // sin, cos of pi q / 512
@@ -352,7 +382,7 @@ __device__ __forceinline__ double2 pre_y(const Lane& c, int m, double2 xa, doubl
 // pre-processed input y_{q + 16 m} of FFT f of warp w
 template <int RAW>
 __device__ __forceinline__ void pre_read(const double2* tile, int w, const Lane& c_in, double2 (&v)[32], double sc,
-                                         int sha = 0, int shb = 0) {
+                                         int sha = 0, int shb = 0, int sp = 512) {
   Lane c = c_in;
   const double hsc = 0.5 * sc;
   const int f = c.f, q = c.q, q7 = q & 7;
@@ -369,9 +399,11 @@ __device__ __forceinline__ void pre_read(const double2* tile, int w, const Lane&
   };
   if constexpr (RAW == RAW_CONTIG) {
     // lines 4w + 2f (real) and 4w + 2f + 1 (imag), row j at j - 1 + shift
-    const double* d = reinterpret_cast<const double*>(tile) + (4 * w + 2 * f) * 512;
+    // lines at 4w*512 + l*sp: sp = 512 (cp.async tiles, per-line shifts) or
+    // the global pitch 511 / 512 (bulk-copied tiles, no shift)
+    const double* d = reinterpret_cast<const double*>(tile) + 4 * w * 512 + 2 * f * sp;
     const double* ra = d + sha - 1;
-    const double* rb = d + 512 + shb - 1;
+    const double* rb = d + sp + shb - 1;
 #pragma unroll
     for (int m = 0; m < 32; ++m) {
       batch(m);
@@ -766,6 +798,7 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
   double2* const tile = smem_grp;
   double2* const scr_all = smem_grp + TILE;
   uint64_t* const bar = reinterpret_cast<uint64_t*>(scr_all + NWARP * SCR);
+  uint64_t* const wbar = bar + 1 + (threadIdx.x >> 5);  // per-warp barrier of bulk line copies
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* const scr = scr_all + SCR * w;
   const uint32_t stile = smem_u32(tile);
@@ -781,9 +814,17 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
     } else if constexpr (STRIDED) {
       issue_strided<SIDE_IN>(a, tt, stile, w, lane);
     } else {
-      issue_contig(a, tt, stile, w, lane);
+      issue_contig_any(a, tt, tile, stile, w, lane, wbar);
     }
   };
+  uint32_t wphase = 0;
+  if constexpr (!STRIDED) {
+    if (lane == 0) {
+      mbar_init(wbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+  }
   if constexpr (TMA) {
     if ((stile & 1023u) != 0) __trap();  // the 128-byte swizzle needs a 1024-byte aligned tile
     if (threadIdx.x == 0) {
@@ -800,18 +841,24 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
       if (!(FL_REG_NOMEM == 1 || FL_REG_NOMEM == 2)) mbar_wait(bar, phase);
       phase ^= 1;
     }
+    int sha = 0, shb = 0, sp = 512;  // contiguous tiles: line shifts and smem line pitch
+    if constexpr (!STRIDED) {
+      const Tile tin = tile_of<SIDE_CONTIG, false>(a, t);
+      if (contig_bulk(a, tin, w)) {
+        if (!(FL_REG_NOMEM == 1 || FL_REG_NOMEM == 2)) mbar_wait(wbar, wphase);
+        wphase ^= 1;
+        sp = (int)tin.LS;
+      } else {
+        sha = line_shift(tin, 4 * w + 2 * (lane >> 4));
+        shb = line_shift(tin, 4 * w + 2 * (lane >> 4) + 1);
+      }
+    }
     cp_wait<0>();
     if (STRIDED) __syncthreads(); else __syncwarp();
     double2 v[32], ev[16], od[16];
-    int sha = 0, shb = 0;  // contiguous tiles: alignment shifts of the warp's lines 4w + 2f, 4w + 2f + 1
-    if constexpr (!STRIDED) {
-      const Tile tin = tile_of<SIDE_CONTIG, false>(a, t);
-      sha = line_shift(tin, 4 * w + 2 * (lane >> 4));
-      shb = line_shift(tin, 4 * w + 2 * (lane >> 4) + 1);
-    }
     if constexpr (!MID) {
       const Lane c = lane_consts(a, lane);
-      pre_read<STRIDED ? RAW_STRIDED : RAW_CONTIG>(tile, w, c, v, 0.5 * a.scale, sha, shb);
+      pre_read<STRIDED ? RAW_STRIDED : RAW_CONTIG>(tile, w, c, v, 0.5 * a.scale, sha, shb, sp);
       if (STRIDED) __syncthreads(); else __syncwarp();
       if (tn < ntiles) issue_next(tn);
       cp_commit();
@@ -825,14 +872,14 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
         // the back edge
         if (ph == 0) {
           pre_read<STRIDED ? RAW_STRIDED : RAW_CONTIG>(tile, w, lane_consts<true>(a, lane), v, 0.25 * a.scale, sha,
-                                                       shb);
+                                                       shb, sp);
         } else {
           pre_read<RAW_Z>(tile, w, lane_consts<true>(a, lane), v, 1.0);
         }
         // phase 0: the tile is consumed, quarter w (16 KB) is the warp's own
         // from here; phase 1: every warp has read its z, the tile is free (z
         // was written through the generic proxy: fence before TMA refills it)
-        if (TMA && ph == 1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if ((TMA || !STRIDED) && ph == 1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         if (STRIDED) __syncthreads(); else __syncwarp();
         if (ph == 0) {
           // bring the unit's lane-ordered core slice into quarter w while the
@@ -895,7 +942,7 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
   if (TST && threadIdx.x == 0) bulk_wait_all();
 }
 
-constexpr size_t grp_smem_bytes() { return (size_t)(TILE + NWARP * SCR) * sizeof(double2) + 16; }
+constexpr size_t grp_smem_bytes() { return (size_t)(TILE + NWARP * SCR) * sizeof(double2) + 8 * (1 + NWARP) + 8; }
 
 }  // namespace rg
 }  // namespace fl
