@@ -818,7 +818,7 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
     }
   };
   uint32_t wphase = 0;
-  if constexpr (!STRIDED) {
+  if constexpr (!STRIDED || MID) {
     if (lane == 0) {
       mbar_init(wbar, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -884,15 +884,12 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
         if (ph == 0) {
           // bring the unit's lane-ordered core slice into quarter w while the
           // forward FFT runs
-          if (!FL_REG_NOMEM) {
-            const double2* cl = reinterpret_cast<const double2*>(a.core) + (size_t)(4 * t + w) * 1024 + lane;
-            const uint32_t d = stile + 16u * (uint32_t)(1024 * w + lane);
-            static_for<0, 32>([&](auto I) {
-              constexpr int i = decltype(I)::value;
-              cp16<16 * 32 * i>(d, cl + 32 * i, 16);
-            });
+          // (one bulk copy: the slice is 16 KB contiguous in lane order)
+          if (lane == 0 && !FL_REG_NOMEM) {
+            mbar_expect_tx(wbar, 16384u);
+            bulk_load(tile + 1024 * w, reinterpret_cast<const double2*>(a.core) + (size_t)(4 * t + w) * 1024, 16384u,
+                      wbar);
           }
-          cp_commit();
         } else {
           if (tn < ntiles) issue_next(tn);
           cp_commit();
@@ -903,7 +900,8 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
           // z = S' .* core for rows 2k, 2k+1 (k = 16 q + i): multiply in
           // registers (core entry (i', lane) at 32 i' + lane), then write z
           // over the core in the z layout
-          cp_wait<0>();
+          if (!FL_REG_NOMEM) mbar_wait(wbar, wphase);
+          wphase ^= 1;
           __syncwarp();
           const double2* cw = tile + 1024 * w + lane;
 #pragma unroll
