@@ -1,5 +1,6 @@
 // Host side of the DST-I transforms: per-length tables, kernel dispatch,
 // and the dense sine-matrix path for lengths without an FFT plan.
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <map>
@@ -126,17 +127,21 @@ namespace {
 template <typename K>
 int grid_for(K kernel, int nt, size_t smem, int64_t ntiles, int* grid) {
   static std::mutex mu;
-  static std::map<const void*, int> occ;
+  // keyed by (device, kernel): function attributes are set per device
+  static std::map<std::pair<int, const void*>, int> occ;
   int blocks = 0;
+  int dev = 0;
+  FL_CUDA_TRY(cudaGetDevice(&dev));
   {
     std::lock_guard<std::mutex> lk(mu);
-    auto it = occ.find((const void*)kernel);
+    const auto key = std::make_pair(dev, (const void*)kernel);
+    auto it = occ.find(key);
     if (it == occ.end()) {
       if (smem > 48 * 1024)
         FL_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       FL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, nt, smem));
       if (blocks < 1) blocks = 1;
-      occ[(const void*)kernel] = blocks;
+      occ[key] = blocks;
     } else {
       blocks = it->second;
     }
@@ -238,10 +243,14 @@ template <int SIN, int SOUT, bool MID, bool TMA, bool TST>
 int launch_reg_k(const DstArgs& a, const CUtensorMap& map, const rg::OutMaps& om, cudaStream_t st) {
   auto kern = rg::k_dst_grp<SIN, SOUT, MID, TMA, TST>;
   constexpr size_t SMEM = rg::grp_smem_bytes();
-  static bool attr = false;
-  if (!attr) {
+  // function attributes are per device: one flag bit per device ordinal
+  static std::atomic<uint64_t> attr_set{0};
+  int dev = 0;
+  FL_CUDA_TRY(cudaGetDevice(&dev));
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  if (!(attr_set.load() & bit)) {
     FL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
-    attr = true;
+    attr_set.fetch_or(bit);
   }
   const int64_t cap = 2 * (int64_t)sm_count();
   const int grid = (int)(a.ntiles < cap ? a.ntiles : cap);

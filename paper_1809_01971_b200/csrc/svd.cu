@@ -10,6 +10,7 @@
 // Sweeps repeat until no pair has |a_p . a_q| > tol sqrt(|a_p|^2 |a_q|^2).
 // Then sigma_j = |a_j|, u_j = a_j / sigma_j, V = accumulated rotations;
 // outputs are sorted by decreasing sigma.
+#include <atomic>
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -170,10 +171,14 @@ int svd_batched(const double* A, int batch, int m, int n, double* U, double* S, 
   const size_t smem = (w_sm ? wb : 0) + (v_sm ? vb : 0) + tail;
   double* scratch = nullptr;
   if (!(w_sm && v_sm)) FL_CUDA_TRY(cudaMallocAsync(&scratch, (wb + vb) * (size_t)batch, st));
-  static bool attr_set = false;
-  if (!attr_set) {
+  // function attributes are per device: one flag bit per device ordinal
+  static std::atomic<uint64_t> attr_set{0};
+  int dev = 0;
+  FL_CUDA_TRY(cudaGetDevice(&dev));
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  if (!(attr_set.load() & bit)) {
     FL_CUDA_TRY(cudaFuncSetAttribute(k_svd_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SVD_SMEM_CAP));
-    attr_set = true;
+    attr_set.fetch_or(bit);
   }
   k_svd_jacobi<<<batch, SVD_THREADS, smem, st>>>(A, m, n, U, S, Vt, 40, scratch, w_sm, v_sm);
   FL_LAUNCH_CHECK();
