@@ -539,6 +539,10 @@ __device__ __forceinline__ void fft_split(double2* scr, const Lane& c, double2 (
 // in its warp's scratch, then the CTA writes whole row segments.  Row
 // r' = r0 + 16 s of the half (r0 = 4w + rho lane-constant) sits at
 // sidx(r', f', w') = 32 s + (b ^ ((s >> 1) & 7)) with b lane-constant.
+// strided output, half hh (rows [256 hh, 256 hh + 256)): stage the lane's rows
+// in its warp's scratch, then the CTA writes whole row segments.  Row
+// r' = r0 + 16 s of the half (r0 = 4w + rho lane-constant) sits at
+// sidx(r', f', w') = 32 s + (b ^ ((s >> 1) & 7)) with b lane-constant.
 #ifndef FL_REG_DIRECT_STORE
 #define FL_REG_DIRECT_STORE 0
 #endif
@@ -927,8 +931,6 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
     if constexpr (STRIDED) {
       if constexpr (TST) {
         store_strided_tma(a, &omaps, t, scr_all, w, lane >> 4, lane & 15, ev, od);
-      } else if (FL_REG_DIRECT_STORE) {
-        store_strided_direct<SIDE_OUT>(a, t, w, lane >> 4, lane & 15, ev, od, sc);
       } else {
         store_strided<SIDE_OUT>(a, t, scr_all, w, lane, lane >> 4, lane & 15, ev, od, sc);
       }
