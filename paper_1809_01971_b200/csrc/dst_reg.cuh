@@ -539,48 +539,6 @@ __device__ __forceinline__ void fft_split(double2* scr, const Lane& c, double2 (
 // in its warp's scratch, then the CTA writes whole row segments.  Row
 // r' = r0 + 16 s of the half (r0 = 4w + rho lane-constant) sits at
 // sidx(r', f', w') = 32 s + (b ^ ((s >> 1) & 7)) with b lane-constant.
-// strided output, half hh (rows [256 hh, 256 hh + 256)): stage the lane's rows
-// in its warp's scratch, then the CTA writes whole row segments.  Row
-// r' = r0 + 16 s of the half (r0 = 4w + rho lane-constant) sits at
-// sidx(r', f', w') = 32 s + (b ^ ((s >> 1) & 7)) with b lane-constant.
-#ifndef FL_REG_DIRECT_STORE
-#define FL_REG_DIRECT_STORE 0
-#endif
-// strided output straight from registers: lane (f, q) writes rows 32q + 2i
-// (+1) of its line pair, 16 bytes per row; a warp instruction covers 16 rows
-// x 32 bytes (sector-complete), no staging and no CTA barrier
-template <int SIDE_OUT>
-__device__ __forceinline__ void store_strided_direct(const DstArgs& a, uint32_t t, int w, int f, int q,
-                                                     const double2 (&ev)[16], const double2 (&od)[16], double sc) {
-  const Tile tl = tile_of<SIDE_OUT, true>(a, t);
-  const int col = 4 * w + 2 * f;
-  const bool va = col < tl.lmax, vb = col + 1 < tl.lmax;
-  double* p = a.y + tl.base + col + (int64_t)(32 * q) * tl.JS;  // odd row 32q + 2i + 1 at 32q + 2i
-  const int64_t JS = tl.JS, JS2 = 2 * tl.JS;
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const double2 e = make_double2(sc * ev[i].x, sc * ev[i].y);
-    const double2 o = make_double2(sc * od[i].x, sc * od[i].y);
-    double* pe = p - JS;
-    if (SIDE_OUT == SIDE_VEC) {
-      if (va) {
-        if (i > 0 || q > 0) *reinterpret_cast<double2*>(pe) = e;
-        *reinterpret_cast<double2*>(p) = o;
-      }
-    } else {
-      if (va) {
-        if (i > 0 || q > 0) pe[0] = e.x;
-        p[0] = o.x;
-      }
-      if (vb) {
-        if (i > 0 || q > 0) pe[1] = e.y;
-        p[1] = o.y;
-      }
-    }
-    p += JS2;
-  }
-}
-
 template <int SIDE_OUT>
 __device__ __forceinline__ void store_strided(const DstArgs& a, uint32_t t, double2* scr_all, int w, int lane, int f,
                                               int q, const double2 (&ev)[16], const double2 (&od)[16], double sc) {
