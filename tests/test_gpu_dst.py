@@ -228,7 +228,7 @@ def test_apply_full_lanes_matches_oracle(dims):
     the oracle and vs the padded path with the natural core layout."""
     spec = spectral.EigenSpectrum(tuple(spectral.laplacian_mode(n) for n in dims))
     kind = CoreFunctionKind("g2", 0.75, coeff_minus=1.3, coeff_plus=0.7)
-    op = full.FullOperator.from_kind(kind, spec)
+    op = full.FullOperator(spec, full.dense_core(kind, spec), lanes=True)
     assert op.lanes and op.padded and op.core_l is not None
     core_want = oracle.dense_core("g2", [oracle.laplacian_eigenvalues(n) for n in dims], 0.75, 1.3, 0.7)
     assert rel(op.core.cpu().numpy(), core_want) <= 1e-14
