@@ -259,3 +259,42 @@ def test_dst1_pass_n511_many_tiles_per_cta(blocks, inplace):
     lay = (n * P, P, 0, 0)
     full.run_pass((_lib.ptr(x), _lib.ptr(y), None, n, 0, blocks, 1, P, lay, lay, 1.0))
     assert rel(y.cpu().numpy(), want) <= 1e-13
+
+
+@pytest.mark.parametrize("width,groups,pad", [(5, 3, 0), (37, 2, 3), (16, 1, 0), (40, 2, 2), (511, 1, 1)])
+def test_dst1_pass_n511_strided_layouts(width, groups, pad):
+    """n = 511 strided passes through the register kernel with partial
+    16-column chunks, odd widths (scalar sides), several groups and distinct
+    input/output layouts; padding columns of the output stay untouched."""
+    from paper_1809_01971_b200 import _lib
+    n, blocks = 511, 2
+    rng = np.random.default_rng(width * 7 + groups)
+    x = rng.standard_normal((blocks, n, groups, width))
+    want = oracle.dst(x, axis=1)
+    xt = torch.tensor(x, device="cuda")
+    wo = width + pad
+    yt = torch.full((blocks, groups, n, wo), 7.0, dtype=torch.float64, device="cuda")
+    lin = (n * groups * width, groups * width, width, 0)
+    lout = (groups * n * wo, wo, n * wo, 0)
+    full.run_pass((_lib.ptr(xt), _lib.ptr(yt), None, n, 0, blocks, groups, width, lin, lout, 0.5))
+    got = yt.cpu().numpy()
+    assert rel(got[..., :width], 0.5 * want.transpose(0, 2, 1, 3)) <= 1e-13
+    assert np.all(got[..., width:] == 7.0)
+
+
+@pytest.mark.parametrize("lines,pin,pout", [(1, 511, 512), (17, 511, 511), (33, 512, 515), (100, 515, 512), (16, 512, 512)])
+def test_dst1_pass_n511_contiguous(lines, pin, pout):
+    """n = 511 contiguous passes through the register kernel: dense (511),
+    padded (512) and odd (515) pitches on either side, ragged line counts
+    (bulk copies for whole 4-line units, cp.async with zero fill otherwise)."""
+    from paper_1809_01971_b200 import _lib
+    n = 511
+    rng = np.random.default_rng(lines + pin)
+    x = rng.standard_normal((lines, pin))
+    want = oracle.dst(x[:, :n], axis=1)
+    xt = torch.tensor(x, device="cuda")
+    yt = torch.full((lines, pout), 7.0, dtype=torch.float64, device="cuda")
+    full.run_pass((_lib.ptr(xt), _lib.ptr(yt), None, n, 1, lines, 1, 1, (0, 1, 0, pin), (0, 1, 0, pout), 1.0))
+    got = yt.cpu().numpy()
+    assert rel(got[:, :n], want) <= 1e-13
+    assert np.all(got[:, n:] == 7.0)
