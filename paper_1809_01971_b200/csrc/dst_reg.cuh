@@ -445,8 +445,11 @@ __device__ __forceinline__ void pre_read(const double2* tile, int w, const Lane&
 // 8 KB scratch.  On return ev[i] = S'_{2k}, od[i] = S'_{2k+1} for
 // k = 16 q + i, S' = 2 * DST_raw (lines 2f / 2f+1 in .x / .y; ev[0] of lane
 // 0 is S_0, unused).
+#ifndef FL_REG_TWTAB
+#define FL_REG_TWTAB 0
+#endif
 __device__ __forceinline__ void fft_split(double2* scr, const Lane& c, double2 (&v)[32], double2 (&ev)[16],
-                                          double2 (&od)[16]) {
+                                          double2 (&od)[16], const double2* twt = nullptr) {
   const int f = c.f, q = c.q, q7 = q & 7;
   double2* sf = scr + f * 256;
   dif<32>(v);
@@ -463,9 +466,14 @@ __device__ __forceinline__ void fft_split(double2* scr, const Lane& c, double2 (
       for (int l = 0; l < 8; ++l) {
         const int k2 = 8 * h + l;
         double2 val = v[brev(k2, 5)];
-        if (h == 0 && l == 1) t = c.w1;
-        if ((h == 0 && l >= 2) || (h > 0 && l >= 1)) t = cmul(t, c.w1);
-        if (k2) val = cmul(val, t);
+        if (FL_REG_TWTAB) {
+          // exact W_512^{q k2} from the CTA's table (k2-major, q fastest)
+          if (k2) val = cmul(val, twt[k2 * 16 + q]);
+        } else {
+          if (h == 0 && l == 1) t = c.w1;
+          if ((h == 0 && l >= 2) || (h > 0 && l >= 1)) t = cmul(t, c.w1);
+          if (k2) val = cmul(val, t);
+        }
         const int kk = k2 & 15;
         sf[kk * 16 + (q ^ (kk & 7))] = val;
       }
@@ -761,6 +769,11 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
   double2* const scr_all = smem_grp + TILE;
   uint64_t* const bar = reinterpret_cast<uint64_t*>(scr_all + NWARP * SCR);
   uint64_t* const wbar = bar + 1 + (threadIdx.x >> 5);  // per-warp barrier of bulk line copies
+  double2* const twt = scr_all + NWARP * SCR + 4;        // FL_REG_TWTAB: W_512^{q k2}, [k2][q]
+  if (FL_REG_TWTAB) {
+    for (int i = threadIdx.x; i < 512; i += 32 * NWARP) twt[i] = __ldg(&a.tw[((i & 15) * (i >> 4)) & (N - 1)]);
+    __syncthreads();
+  }
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* const scr = scr_all + SCR * w;
   const uint32_t stile = smem_u32(tile);
@@ -824,7 +837,7 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
       if (STRIDED) __syncthreads(); else __syncwarp();
       if (tn < ntiles) issue_next(tn);
       cp_commit();
-      fft_split(scr, c, v, ev, od);
+      fft_split(scr, c, v, ev, od, twt);
     } else {
       // forward, core, inverse: a rolled loop keeps one copy of the FFT code
       // (two inlined copies do not fit the register file)
@@ -857,7 +870,7 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
           cp_commit();
         }
         // shared addressing survives: the laundered part is an integer offset
-        fft_split(scr_all + launder_i(SCR * w), lane_consts<true>(a, lane), v, ev, od);
+        fft_split(scr_all + launder_i(SCR * w), lane_consts<true>(a, lane), v, ev, od, twt);
         if (ph == 0) {
           // z = S' .* core for rows 2k, 2k+1 (k = 16 q + i): multiply in
           // registers (core entry (i', lane) at 32 i' + lane), then write z
@@ -900,7 +913,9 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
   if (TST && threadIdx.x == 0) bulk_wait_all();
 }
 
-constexpr size_t grp_smem_bytes() { return (size_t)(TILE + NWARP * SCR) * sizeof(double2) + 8 * (1 + NWARP) + 8; }
+constexpr size_t grp_smem_bytes() {
+  return (size_t)(TILE + NWARP * SCR + 4 + (FL_REG_TWTAB ? 512 : 0)) * sizeof(double2);
+}
 
 }  // namespace rg
 }  // namespace fl
