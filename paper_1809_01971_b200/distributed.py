@@ -11,8 +11,10 @@ the spectral layout, so the PCG iteration (three streaming phases per
 iteration) needs only 3 scalar all-reduces per iteration; the two all-to-alls
 happen once per solve (b -> b_hat, x_hat -> x).
 
-The compute primitives come from a `LocalOps` object; `CudaOps` binds them to
-libfraclap_b200 (the product).  Tests substitute a host implementation to
+The compute primitives come from a `LocalOps` object (each returns a new
+tensor and leaves its input untouched); `CudaOps` binds them to
+libfraclap_b200 (the product; the first DST pass of each primitive writes out
+of place, so no defensive copies are made).  Tests substitute a host implementation to
 exercise the decomposition, transposes and reduction logic with gloo on CPU.
 """
 
@@ -62,22 +64,27 @@ class CudaOps:
     """Local compute through libfraclap_b200 (device tensors)."""
 
     def dst_inner_modes(self, x, n1, n2):
-        """DST-I along modes 2 and 1 of a (m, n1, n2) slab, in place."""
+        """DST-I along modes 2 and 1 of a (m, n1, n2) slab into a new tensor
+        (x is not modified; the first pass writes out of place, so no copy)."""
         m = x.shape[0]
         st = _lib.stream_ptr()
         if m == 0:
-            return x
-        _lib.call("fl_dst1", _lib.ptr(x), _lib.ptr(x), m * n1, n2, 1, 1.0, st)
-        _lib.call("fl_dst1", _lib.ptr(x), _lib.ptr(x), m, n1, n2, 1.0, st)
-        return x
+            return x.clone()
+        x = x.contiguous()
+        y = torch.empty_like(x)
+        _lib.call("fl_dst1", _lib.ptr(x), _lib.ptr(y), m * n1, n2, 1, 1.0, st)
+        _lib.call("fl_dst1", _lib.ptr(y), _lib.ptr(y), m, n1, n2, 1.0, st)
+        return y
 
     def dst_mode0(self, y, scale=1.0):
-        """DST-I along mode 0 of a (n0, m, n2) slab, in place."""
+        """DST-I along mode 0 of a (n0, m, n2) slab into a new tensor."""
         n0, m, n2 = y.shape
         if m * n2 == 0:
-            return y
-        _lib.call("fl_dst1", _lib.ptr(y), _lib.ptr(y), 1, n0, m * n2, float(scale), _lib.stream_ptr())
-        return y
+            return y.clone()
+        y = y.contiguous()
+        out = torch.empty_like(y)
+        _lib.call("fl_dst1", _lib.ptr(y), _lib.ptr(out), 1, n0, m * n2, float(scale), _lib.stream_ptr())
+        return out
 
     def pcg_phase(self, phase, b, x, r, p, A, P, s, out, work):
         _lib.call("fl_pcg_phase", phase, _lib.ptr(b), _lib.ptr(x), _lib.ptr(r), _lib.ptr(p), _lib.ptr(A),
@@ -109,7 +116,8 @@ def transpose_bwd(y, lay, group=None):
     """(n0, |S_r|, n2) -> (|X_r|, n1, n2)."""
     n0, n1, n2 = lay.dims
     ls = y.shape[1]
-    send = torch.cat([y[s:e].reshape(-1) for (s, e) in lay.X])
+    # the nodal ranges X partition axis 0 in order: the send buffer is y itself
+    send = y.contiguous().reshape(-1)
     m = lay.X[lay.rank][1] - lay.X[lay.rank][0]
     recv = y.new_empty(m * n1 * n2)
     _a2a(recv, send, [m * (e - s) * n2 for (s, e) in lay.S], [(e - s) * ls * n2 for (s, e) in lay.X], group)
@@ -124,13 +132,13 @@ def transpose_bwd(y, lay, group=None):
 
 def transform_fwd(x, lay, ops, group=None):
     """Full orthonormal DST-I of a nodal slab -> spectral slab."""
-    x = ops.dst_inner_modes(x.clone(), lay.dims[1], lay.dims[2])
+    x = ops.dst_inner_modes(x, lay.dims[1], lay.dims[2])  # new tensor, x untouched
     return ops.dst_mode0(transpose_fwd(x, lay, group).contiguous())
 
 
 def transform_bwd(y, lay, ops, scale=1.0, group=None):
     """Inverse of transform_fwd (DST-I is involutive)."""
-    y = ops.dst_mode0(y.clone(), scale)
+    y = ops.dst_mode0(y, scale)  # new tensor, y untouched
     return ops.dst_inner_modes(transpose_bwd(y, lay, group), lay.dims[1], lay.dims[2])
 
 
