@@ -203,6 +203,9 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(K) : "memory");
 }
 
+// generic <-> async proxy fence for this CTA's shared memory
+__device__ __forceinline__ void proxy_fence_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 // compiler-only fence: keeps the scheduler from hoisting a whole phase's
 // loads (64 x 16 B in flight would need every register)
 __device__ __forceinline__ void sched_fence() { asm volatile("" ::: "memory"); }
@@ -834,6 +837,10 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
     if constexpr (!MID) {
       const Lane c = lane_consts(a, lane);
       pre_read<STRIDED ? RAW_STRIDED : RAW_CONTIG>(tile, w, c, v, 0.5 * a.scale, sha, shb, sp);
+      // the tile's generic-proxy reads must be ordered before the async-proxy
+      // refill (TMA / bulk copy / cp.async into the same bytes): bar.sync
+      // alone orders only the generic proxy
+      proxy_fence_async();
       if (STRIDED) __syncthreads(); else __syncwarp();
       if (tn < ntiles) issue_next(tn);
       cp_commit();
@@ -852,9 +859,11 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
           pre_read<RAW_Z>(tile, w, lane_consts<true>(a, lane), v, 1.0);
         }
         // phase 0: the tile is consumed, quarter w (16 KB) is the warp's own
-        // from here; phase 1: every warp has read its z, the tile is free (z
-        // was written through the generic proxy: fence before TMA refills it)
-        if ((TMA || !STRIDED) && ph == 1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        // from here; phase 1: every warp has read its z, the tile is free.
+        // Either way the next writes into these bytes come from the async
+        // proxy (core slice / TMA / bulk refill): fence the generic-proxy
+        // reads (and phase 1's z writes) first
+        proxy_fence_async();
         if (STRIDED) __syncthreads(); else __syncwarp();
         if (ph == 0) {
           // bring the unit's lane-ordered core slice into quarter w while the
