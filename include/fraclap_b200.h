@@ -153,8 +153,10 @@ int fl_dst1_core_lanes(const double* x, double* y, const double* core_l, int64_t
  * flag word: FL_PASS_CONTIG selects contiguous lines; FL_PASS_PAD_WRITE
  * lets a strided pass with an odd width write the column after each group
  * (the padding of an internal work buffer, as in fl_apply_full_padded)
- * so that it can store 16-byte line pairs; without it the padding is never
- * written. */
+ * so that it can store 16-byte line pairs, and makes a contiguous pass with
+ * out pitch > n zero the padding of every line (later strided passes pair
+ * the last column with the padding in one packed FFT, so it must hold a
+ * defined value); without it the padding is never written. */
 #define FL_PASS_CONTIG 1
 #define FL_PASS_PAD_WRITE 2
 int fl_dst1_pass(const double* x, double* y, const double* core, int64_t n, int contig,

@@ -158,7 +158,9 @@ int fl_apply_full_lanes(const double* x, double* y, const double* core_l, double
   cudaStream_t st = as_stream(stream);
   // last mode first, contiguous: dense rows (pitch 511) -> padded rows (512)
   const PassLayout dense_l{0, 1, 0, nl}, pad_l{0, 1, 0, P};
-  if ((rc = dst_pass(x, work, nullptr, nl, true, lines, 1, 1, dense_l, pad_l, 1.0, st))) return rc;
+  // (writes the padding position too: pass 2 and the fused pass pair the last
+  // column with it in one packed FFT)
+  if ((rc = dst_pass(x, work, nullptr, nl, true, lines, 1, 1, dense_l, pad_l, 1.0, st, true))) return rc;
   const PassLayout mid{n1 * P, P, 0, 0};
   if (d == 3 && (rc = dst_pass(work, work, nullptr, n1, false, n0, 1, P, mid, mid, 1.0, st))) return rc;
   // mode 0: forward, core, inverse in one pass

@@ -437,6 +437,7 @@ int dst_pass(const double* x, double* y, const double* core, int64_t n, bool con
   a.core = core;
   a.tw = t->tw;
   a.sn = t->sn;
+  a.pad_zero = (pad_write && contig && out.lp > n) ? 1 : 0;
   if (!contig) {
     // 16-byte line pairs: aligned base and strides; an odd group width is
     // fine when the layout has room for one more column after the last
@@ -453,7 +454,7 @@ int dst_pass(const double* x, double* y, const double* core, int64_t n, bool con
     auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
     if (core == nullptr && contig && in.lp >= 511 && al16(x)) {
       a.scale = scale * nrm;
-      return launch_reg<rg::SIDE_CONTIG, rg::SIDE_CONTIG, false>(a, st);
+      return launch_reg<rg::SIDE_CONTIG, rg::SIDE_CONTIG, false>(a, st);  // zeroes the padding itself
     }
     if (core == nullptr && !contig) {
       a.scale = scale * nrm;
@@ -462,6 +463,14 @@ int dst_pass(const double* x, double* y, const double* core, int64_t n, bool con
       if (a.vec_out) return launch_reg<rg::SIDE_SCALAR, rg::SIDE_VEC, false>(a, st);
       return launch_reg<rg::SIDE_SCALAR, rg::SIDE_SCALAR, false>(a, st);
     }
+  }
+  if (contig && a.pad_zero) {
+    // CTA kernel: clear the padding after the pass (same stream)
+    int rc2 = dst_pass(x, y, core, n, contig, outer, groups, wv, in, out, scale, st, false);
+    if (rc2) return rc2;
+    FL_CUDA_TRY(cudaMemset2DAsync(y + n, (size_t)out.lp * sizeof(double), 0, (size_t)(out.lp - n) * sizeof(double),
+                                  (size_t)outer, st));
+    return FL_OK;
   }
   if (core == nullptr) {
     a.scale = scale * nrm;

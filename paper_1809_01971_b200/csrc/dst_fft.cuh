@@ -67,6 +67,10 @@ struct DstArgs {
   // (even strides and offsets, 16-byte aligned base and core): one vector
   // access per pair
   int vec_in, vec_out;
+  // contiguous output into an internal padded buffer (pitch > n): write
+  // zeros into the padding position, so that later passes that pair the
+  // last line/column with the padding see a defined value
+  int pad_zero;
   double scale;             // applied at the final store
   const double* core;       // fused pass: core tensor, same layout as x
   // LOAD_KR: virtual input Z[j][c] = U[j][c / S] * Xs[j][c % S], wv = R*S

@@ -658,12 +658,13 @@ __device__ __forceinline__ void store_contig(const DstArgs& a, uint32_t t, doubl
           for (int s = 0; s < 4; ++s) {
             const int c = lane + 32 * s;  // chunk: positions 2c, 2c + 1 of the half
             const double2 val = *reinterpret_cast<const double2*>(sd + l * 256 + 2 * (c ^ ((c >> 4) & 7)));
-            const bool last = (hh == 1 && c == 127);  // position 511 does not exist
-            if (al && !last) {
-              *reinterpret_cast<double2*>(y + 2 * c) = val;
+            const bool last = (hh == 1 && c == 127);  // position 511 is padding (or absent)
+            if (al && (!last || a.pad_zero)) {
+              *reinterpret_cast<double2*>(y + 2 * c) = last ? make_double2(val.x, 0.0) : val;
             } else {
               y[2 * c] = val.x;
               if (!last) y[2 * c + 1] = val.y;
+              else if (a.pad_zero) y[2 * c + 1] = 0.0;
             }
           }
         }

@@ -255,7 +255,8 @@ class FullOperator:
             lines = dims[0] * n1
             dl, pl = (0, 1, 0, nl), (0, 1, 0, P)
             mid = (n1 * P, P, 0, 0)
-            out = [("dst_mode2", (xp, wp, None, nl, 1, lines, 1, 1, dl, pl, 1.0))]
+            # flags 1 | 2 = contiguous | FL_PASS_PAD_WRITE (the padding position is zeroed)
+            out = [("dst_mode2", (xp, wp, None, nl, 3, lines, 1, 1, dl, pl, 1.0))]
             if len(dims) == 3:
                 out.append(("dst_mode1", (wp, wp, None, n1, 0, dims[0], 1, P, mid, mid, 1.0)))
             out.append(("dst_core_mode0", ("lanes0", wp, wp, cp, n1, 1.0)))

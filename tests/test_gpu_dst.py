@@ -298,3 +298,20 @@ def test_dst1_pass_n511_contiguous(lines, pin, pout):
     got = yt.cpu().numpy()
     assert rel(got[:, :n], want) <= 1e-13
     assert np.all(got[:, n:] == 7.0)
+
+
+def test_apply_lanes_bitwise_deterministic():
+    """n = 511 lane apply: repeated runs, and in place vs out of place, agree
+    bit for bit (the kernels are deterministic; a race or a stale padding
+    column would show up as last-bit differences)."""
+    n = 511
+    op = full.FullOperator.from_kind(CoreFunctionKind("g1", 0.5), spectral.laplacian_spectrum(n, 3))
+    g = torch.Generator(device="cuda")
+    g.manual_seed(17)
+    x = torch.randn((n, n, n), dtype=torch.float64, device="cuda", generator=g)
+    ref = op(x).clone()
+    for _ in range(3):
+        assert torch.equal(op(x), ref)
+    z = x.clone()
+    op(z, out=z)
+    assert torch.equal(z, ref)
