@@ -1123,9 +1123,19 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_fft(const DstArgs a) {
 // >= 32 resident warps per SM where shared memory allows
 template <int LOGN>
 struct DstShape {
-  static constexpr int NFFT = LOGN <= 8 ? 16 : (LOGN >= 12 ? 1 : (8 >> (LOGN - 9)));
-  static constexpr int NT = LOGN >= 13 ? 1024 : (LOGN >= 8 ? 512 : (LOGN <= 5 ? 128 : 256));
-  static constexpr int MINB = LOGN >= 13 ? 1 : (LOGN >= 8 ? 2 : (LOGN <= 5 ? 8 : 4));
+#ifndef FL_NFFT10
+#define FL_NFFT10 8
+#endif
+#ifndef FL_NT10
+#define FL_NT10 512
+#endif
+#ifndef FL_MINB10
+#define FL_MINB10 1
+#endif
+  static constexpr int NFFT =
+      LOGN == 10 ? FL_NFFT10 : (LOGN <= 8 ? 16 : (LOGN >= 12 ? 1 : (8 >> (LOGN - 9))));
+  static constexpr int NT = LOGN == 10 ? FL_NT10 : (LOGN >= 13 ? 1024 : (LOGN >= 8 ? 512 : (LOGN <= 5 ? 128 : 256)));
+  static constexpr int MINB = LOGN == 10 ? FL_MINB10 : (LOGN >= 13 ? 1 : (LOGN >= 8 ? 2 : (LOGN <= 5 ? 8 : 4)));
 #ifndef FL_MID_SPLIT
 #define FL_MID_SPLIT 0
 #endif
