@@ -13,6 +13,7 @@
 #include "dst_fft.cuh"
 #include "dst_tma.cuh"
 #include "dst_reg.cuh"
+#include "dst_reg10.cuh"
 #include "kernels.cuh"
 
 namespace fl {
@@ -218,18 +219,21 @@ bool reg_tensor_map(const DstArgs& a, CUtensorMap* map) {
 }
 
 // the three output maps of the TMA-store phase (dst_reg.cuh, OutMaps)
-bool reg_out_maps(const DstArgs& a, rg::OutMaps* m) {
+bool reg_out_maps(const DstArgs& a, rg::OutMaps* m, int nq = 16) {
   auto enc = tma_encoder();
   if (!enc) return false;
   const uint64_t es = sizeof(double);
   const uint64_t row_b = (uint64_t)a.out_js * es;
-  const uint64_t grp_b = a.groups > 1 ? (uint64_t)a.out_gp * es : row_b * 512;
+  const uint64_t grp_b = a.groups > 1 ? (uint64_t)a.out_gp * es : row_b * 1024;
   const uint64_t out_b = a.outer > 1 ? (uint64_t)a.out_os * es : grp_b * (uint64_t)a.groups;
   if (row_b % 16 || grp_b % 16 || out_b % 16) return false;
-  cuuint64_t dims[5] = {(cuuint64_t)a.wv, 16, 32, (cuuint64_t)a.groups, (cuuint64_t)a.outer};
+  // rows g = 32 qq + ii, qq < nq (= N / 32); halves qq < nq/2 and the rest,
+  // the last qq with 31 rows (row N - 1 does not exist)
+  cuuint64_t dims[5] = {(cuuint64_t)a.wv, (cuuint64_t)nq, 32, (cuuint64_t)a.groups, (cuuint64_t)a.outer};
   cuuint64_t strides[4] = {32 * row_b, row_b, grp_b, out_b};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  const cuuint32_t boxes[3][5] = {{16, 8, 32, 1, 1}, {16, 7, 32, 1, 1}, {16, 1, 31, 1, 1}};
+  const cuuint32_t hq = (cuuint32_t)(nq / 2);
+  const cuuint32_t boxes[3][5] = {{16, hq, 32, 1, 1}, {16, hq - 1, 32, 1, 1}, {16, 1, 31, 1, 1}};
   CUtensorMap* maps[3] = {&m->a, &m->b, &m->c};
   for (int k = 0; k < 3; ++k)
     if (enc(maps[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, a.y, dims, strides, const_cast<cuuint32_t*>(boxes[k]), estr,
@@ -302,6 +306,44 @@ int launch_reg(DstArgs a, cudaStream_t st) {
     if (use && reg_tensor_map(a, &map)) return launch_reg_o<SIN, SOUT, MID, true>(a, map, st);
   }
   return launch_reg_o<SIN, SOUT, MID, false>(a, map, st);
+}
+
+// ---- register-resident N = 1024 passes (dst_reg10.cuh) ---------------------
+// strided: 16-byte aligned both sides (TMA loads and stores); contiguous:
+// aligned x.  Returns 1 when launched, 0 when the pass is not eligible.
+template <int SIN>
+int launch_reg10(DstArgs a, cudaStream_t st) {
+  if (SIN == rg::SIDE_CONTIG) {
+    a.ntiles = (a.outer + 15) / 16;
+    a.nchunks = 1;
+  } else {
+    a.nchunks = (a.wv + 15) / 16;
+    a.ntiles = a.outer * a.groups * a.nchunks;
+  }
+  if (a.ntiles == 0) return 1;
+  if (a.ntiles >= (int64_t(1) << 31)) return 0;
+  CUtensorMap map{};
+  rg::OutMaps om{};
+  if (SIN != rg::SIDE_CONTIG) {
+    a.div_blk = make_fastdiv((uint32_t)(a.groups * a.nchunks));
+    a.div_chunk = make_fastdiv((uint32_t)a.nchunks);
+    if (!reg_tensor_map(a, &map) || !reg_out_maps(a, &om, 32)) return 0;
+  }
+  auto kern = rg10::k_dst_reg10<SIN>;
+  constexpr size_t SMEM = rg10::smem_bytes();
+  static std::atomic<uint64_t> attr_set{0};
+  int dev = 0;
+  FL_CUDA_TRY(cudaGetDevice(&dev));
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  if (!(attr_set.load() & bit)) {
+    FL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    attr_set.fetch_or(bit);
+  }
+  const int64_t cap = (int64_t)sm_count();
+  const int grid = (int)(a.ntiles < cap ? a.ntiles : cap);
+  kern<<<grid, 32 * rg10::NWARP, SMEM, st>>>(a, map, om);
+  FL_LAUNCH_CHECK();
+  return 1;
 }
 
 // ---- TMA-fed strided pass (dst_tma.cuh) ----------------------------------
@@ -449,6 +491,18 @@ int dst_pass(const double* x, double* y, const double* core, int64_t n, bool con
     a.vec_in = al(x) && (core == nullptr || al(core)) && in.os % 2 == 0 && in.gp % 2 == 0 && in.js % 2 == 0 &&
                room(in);
     a.vec_out = al(y) && out.os % 2 == 0 && out.gp % 2 == 0 && out.js % 2 == 0 && (wv % 2 == 0 || (pad_write && room(out)));
+  }
+  if (logn == 10 && reg_enabled() && core == nullptr) {
+    auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+    int r = 0;
+    a.scale = scale * nrm;
+    if (contig && in.lp >= 1023 && in.lp < (1ll << 31) && al16(x)) {
+      r = launch_reg10<rg::SIDE_CONTIG>(a, st);
+    } else if (!contig && a.vec_in && a.vec_out) {
+      r = launch_reg10<rg::SIDE_VEC>(a, st);
+    }
+    if (r < 0) return -r;
+    if (r > 0) return FL_OK;
   }
   if (logn == 9 && reg_enabled()) {
     auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
