@@ -315,3 +315,32 @@ def test_apply_lanes_bitwise_deterministic():
     z = x.clone()
     op(z, out=z)
     assert torch.equal(z, ref)
+
+
+@pytest.mark.parametrize("blocks,width", [(3, 1024), (40, 48), (7, 30)])
+def test_dst1_pass_n1023_strided(blocks, width):
+    """n = 1023 strided passes with 16-byte aligned sides (register-resident
+    N = 1024 kernel: TMA loads and stores, many tiles per CTA) vs scipy."""
+    from paper_1809_01971_b200 import _lib
+    n = 1023
+    g = torch.Generator(device="cuda")
+    g.manual_seed(blocks + width)
+    x = torch.randn((blocks, n, width), dtype=torch.float64, device="cuda", generator=g)
+    want = oracle.dst(x.cpu().numpy(), axis=1)
+    y = torch.full_like(x, 7.0)
+    lay = (n * width, width, 0, 0)
+    full.run_pass((_lib.ptr(x), _lib.ptr(y), None, n, 0, blocks, 1, width, lay, lay, 1.0))
+    assert rel(y.cpu().numpy(), want) <= 1e-13
+
+
+def test_apply_full_padded_n1023():
+    """Padded operator at n_0 = n_last = 1023 (the configs[3] size along two
+    modes): mid passes on the N = 1024 register kernel, vs the oracle."""
+    dims = (1023, 3, 1023)
+    spec = spectral.EigenSpectrum(tuple(spectral.laplacian_mode(n) for n in dims))
+    op = full.FullOperator.from_kind(CoreFunctionKind("g2", 0.75, coeff_minus=1.0, coeff_plus=1.0), spec)
+    assert op.padded and op.pitch == 1024
+    core = oracle.dense_core("g2", [oracle.laplacian_eigenvalues(n) for n in dims], 0.75, 1.0, 1.0)
+    x = np.random.default_rng(1023).standard_normal(dims)
+    got = op(torch.tensor(x, device="cuda")).cpu().numpy()
+    assert rel(got, oracle.apply_full(core, x)) <= 1e-12
