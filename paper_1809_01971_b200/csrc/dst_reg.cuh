@@ -44,14 +44,10 @@ namespace fl {
 namespace rg {
 
 constexpr int N = 512, H = 256;
-constexpr int BUF = 1024;  // double2 per warp buffer (16 KB): 512 rows x 2 FFTs
 #ifndef FL_REG_PRE_BATCH
 #define FL_REG_PRE_BATCH 8
 #endif
 constexpr int PRE_BATCH = FL_REG_PRE_BATCH;
-#ifndef FL_REG_PRE_LAUNDER
-#define FL_REG_PRE_LAUNDER 0
-#endif
 
 // unit sides: 16-byte line pairs on a strided layout, single lines on a
 // strided layout, contiguous lines with an even pitch
@@ -344,12 +340,6 @@ __device__ __forceinline__ int launder_i(int v) {
   asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
   return r;
 }
-template <class T>
-__device__ __forceinline__ T* launder_p(T* p) {
-  T* r;
-  asm volatile("mov.b64 %0, %1;" : "=l"(r) : "l"(p));
-  return r;
-}
 
 // lane constants, re-derived per tile (lane index laundered: the smem
 // offsets computed from q are loop-invariant too)
@@ -394,7 +384,7 @@ __device__ __forceinline__ void pre_read(const double2* tile, int w, const Lane&
   auto batch = [&](int m) {
     if (m % PRE_BATCH == 0) {
       sched_fence();
-      if (RAW != RAW_STRIDED || FL_REG_PRE_LAUNDER) {
+      if (RAW != RAW_STRIDED) {  // (measured: the plain strided pass is faster without)
         c.sq = launder_d(c.sq);
         c.cq = launder_d(c.cq);
       }
