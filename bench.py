@@ -349,7 +349,7 @@ def run_solves(args, rank, world, dev):
     import numpy as np
     import torch
     import paper_1809_01971_b200 as fl
-    from paper_1809_01971_b200 import distributed as D, fullsolve
+    from paper_1809_01971_b200 import distributed as D, fullsolve, full
     from paper_1809_01971_b200.full import cp_dense
 
     out = {}
@@ -390,14 +390,18 @@ def run_solves(args, rank, world, dev):
     def setup():
         pre = fullsolve.kronecker_preconditioner(cfg, spec)
         kind = fullsolve._control_kind(cfg)
-        return D.spectral_core(kind, spec, lay), D.spectral_cp_core(pre.diag.core, lay)
+        A, P = D.spectral_core(kind, spec, lay), D.spectral_cp_core(pre.diag.core, lay)
+        if world == 1 and full.padded_transform_ok(spec):
+            # one GPU: the spectral PCG runs on the padded layout (register-resident transforms)
+            A, P = full.to_padded(A), full.to_padded(P)
+        return A, P
 
     (A, P), t_setup = _dev_time(setup, world)
     ops = D.CudaOps()
     if world == 1:
         (u, rep), t_solve = _dev_time(lambda: fullsolve.solve_control_full(y, cfg, spec, cores=(A, P)), 1)
         its, res = rep.iterations, rep.residuals[-1]
-        path = "spectral PCG, 1 persistent kernel"
+        path = "spectral PCG, 1 persistent kernel (padded spectral layout)"
     else:
         (u, its, hist, conv), t_solve = _dev_time(lambda: D.pcg_slab(y, A, P, lay, ops, cfg.residual_tol, cfg.k_max),
                                                    world)

@@ -23,7 +23,8 @@ from . import _lib
 from .fracop import CoreFunctionKind, mode_values_device
 from .spectral import EigenSpectrum, transform_axis
 
-__all__ = ["FullOperator", "padded_pitch", "run_pass", "dense_core", "apply_full", "transform_full", "apply_host_stream", "inner", "norm"]
+__all__ = ["FullOperator", "padded_pitch", "run_pass", "dense_core", "apply_full", "transform_full", "apply_host_stream", "inner", "norm",
+           "transform_full_padded", "transform_full_from_padded", "to_padded", "padded_transform_ok"]
 
 
 def _shape_check(spectrum, x):
@@ -97,6 +98,77 @@ def transform_full(spectrum, x, direction="forward", alpha=1.0, out=None):
         z = transform_axis(m, z.contiguous(), direction, ax)
     y.copy_(z * alpha if alpha != 1.0 else z)
     return y
+
+
+def padded_transform_ok(spectrum):
+    """Whether the padded spectral layout (last mode of pitch padded_pitch(n))
+    applies: sine modes of FFT length, d = 2 or 3, last mode not a multiple
+    of 16."""
+    dims = tuple(spectrum.mode_sizes)
+    return (spectrum.all_sine and len(dims) in (2, 3) and all(_fft_length(n) for n in dims)
+            and dims[-1] % 16 != 0)
+
+
+def _padded_passes(dims, P):
+    """(first contiguous pass layouts, strided passes) of the padded transform."""
+    nl = dims[-1]
+    lines = 1
+    for n in dims[:-1]:
+        lines *= n
+    strided = []
+    if len(dims) == 3:
+        n0, n1 = dims[0], dims[1]
+        mid = (n1 * P, P, 0, 0)
+        strided.append((n1, n0, 1, P, mid))
+        strided.append((n0, 1, n1, P, (0, n1 * P, P, 0)))
+    else:
+        strided.append((dims[0], 1, 1, P, (0, P, 0, 0)))
+    return lines, strided
+
+
+def transform_full_padded(spectrum, x):
+    """F x for a dense x, returned in the padded layout (last mode of pitch
+    padded_pitch(n), padding zero): the last mode as contiguous lines (dense
+    rows -> padded rows), then the other modes on aligned strided layouts, so
+    every pass can run on the register-resident kernels."""
+    _check_operand(x)
+    _shape_check(spectrum, x)
+    dims = tuple(spectrum.mode_sizes)
+    nl, P = dims[-1], padded_pitch(dims[-1])
+    out = torch.empty(dims[:-1] + (P,), dtype=torch.float64, device=x.device)
+    lines, strided = _padded_passes(dims, P)
+    xp, op_ = _lib.ptr(x), _lib.ptr(out)
+    # flag 3 = contiguous | FL_PASS_PAD_WRITE: the padding is zeroed
+    run_pass((xp, op_, None, nl, 3, lines, 1, 1, (0, 1, 0, nl), (0, 1, 0, P), 1.0))
+    for n, outer, groups, width, lay in reversed(strided):
+        run_pass((op_, op_, None, n, 0, outer, groups, width, lay, lay, 1.0))
+    out[..., nl:].zero_()  # the strided passes leave rounding noise in the padding
+    return out
+
+
+def transform_full_from_padded(spectrum, xp, alpha=1.0, out=None):
+    """Inverse of transform_full_padded (F is involutive): xp (padded layout,
+    consumed: transformed in place) -> dense alpha * F xp."""
+    dims = tuple(spectrum.mode_sizes)
+    nl, P = dims[-1], padded_pitch(dims[-1])
+    if tuple(xp.shape) != dims[:-1] + (P,) or not xp.is_contiguous():
+        raise ValueError("expected a contiguous padded-layout tensor of shape %r" % (dims[:-1] + (P,),))
+    y = out if out is not None else torch.empty(dims, dtype=torch.float64, device=xp.device)
+    lines, strided = _padded_passes(dims, P)
+    p_ = _lib.ptr(xp)
+    for n, outer, groups, width, lay in strided:
+        run_pass((p_, p_, None, n, 0, outer, groups, width, lay, lay, 1.0))
+    run_pass((p_, _lib.ptr(y), None, nl, 1, lines, 1, 1, (0, 1, 0, P), (0, 1, 0, nl), float(alpha)))
+    return y
+
+
+def to_padded(t, fill=0.0):
+    """Copy of a dense tensor in the padded layout (padding = fill)."""
+    dims = tuple(t.shape)
+    P = padded_pitch(dims[-1])
+    out = torch.full(dims[:-1] + (P,), float(fill), dtype=torch.float64, device=t.device)
+    out[..., :dims[-1]].copy_(t)
+    return out
 
 
 def _fft_length(n):

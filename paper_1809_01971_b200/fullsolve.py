@@ -18,7 +18,8 @@ import torch
 
 from . import _lib
 from .fracop import CoreFunctionKind, dense_core_dev
-from .full import apply_full, cp_dense, dense_core, transform_full
+from .full import (apply_full, cp_dense, dense_core, padded_pitch, padded_transform_ok, to_padded, transform_full,
+                   transform_full_from_padded, transform_full_padded)
 from .solver import PcgBreakdownError, PcgReport, SolverConfig, build_preconditioner
 
 __all__ = ["control_cores", "pcg_full", "solve_control_full", "solve_state_full"]
@@ -28,11 +29,13 @@ def _control_kind(cfg):
     return CoreFunctionKind("g2", cfg.alpha, coeff_minus=float(cfg.beta), coeff_plus=float(cfg.gamma) / float(cfg.beta))
 
 
-def control_cores(cfg, spectrum, precond="kronecker", seed=0):
+def control_cores(cfg, spectrum, precond="kronecker", seed=0, layout="dense"):
     """Dense system core A = g2(beta, gamma/beta) and preconditioner core P.
 
     precond: "kronecker" (the reference's rank-r reciprocal core, expanded to
-    dense), "exact" (1/g2, i.e. g3), or "identity".
+    dense), "exact" (1/g2, i.e. g3), or "identity".  layout="padded" returns
+    them in the padded layout (zero padding) that pcg_full runs on with the
+    register-resident transforms (when padded_transform_ok(spectrum)).
     """
     kind = _control_kind(cfg)
     A = dense_core(kind, spectrum)
@@ -45,6 +48,10 @@ def control_cores(cfg, spectrum, precond="kronecker", seed=0):
         P = torch.ones_like(A)
     else:
         raise ValueError("precond must be 'kronecker', 'exact' or 'identity'")
+    if layout == "padded" and padded_transform_ok(spectrum):
+        return to_padded(A), to_padded(P)
+    if layout not in ("dense", "padded"):
+        raise ValueError("layout must be 'dense' or 'padded'")
     return A, P
 
 
@@ -65,12 +72,26 @@ def pcg_full(spectrum, A, P, b, tol, k_max, mode="spectral"):
     <P,S> <= 0 exactly as the reference (solver.py:154-159).
     """
     if mode == "nodal":
+        nl = spectrum.mode_sizes[-1]
+        if A.shape[-1] != nl:  # padded-layout cores: the literal iteration wants dense ones
+            A, P = A[..., :nl].contiguous(), P[..., :nl].contiguous()
         return _pcg_nodal(spectrum, A, P, b, tol, k_max)
     if mode != "spectral":
         raise ValueError("mode must be 'spectral' or 'nodal'")
     dev = b.device
-    N = b.numel()
-    bh = transform_full(spectrum, b)
+    dims = tuple(spectrum.mode_sizes)
+    padded = padded_transform_ok(spectrum) and tuple(A.shape) == dims[:-1] + (padded_pitch(dims[-1]),)
+    if padded:
+        # cores in the padded layout (zero padding): the iteration runs on
+        # padded spectral coefficients (the padding stays zero: P_pad = 0 keeps
+        # the search directions there at zero), both transforms on the
+        # register-resident kernels
+        if tuple(P.shape) != tuple(A.shape):
+            raise ValueError("A and P must share the (padded) layout")
+        bh = transform_full_padded(spectrum, b)
+    else:
+        bh = transform_full(spectrum, b)
+    N = bh.numel()
     xh = torch.empty_like(bh)
     r = torch.empty_like(bh)
     p = torch.empty_like(bh)
@@ -82,7 +103,7 @@ def pcg_full(spectrum, A, P, b, tol, k_max, mode="spectral"):
     _lib.call("fl_pcg_spectral", _lib.ptr(bh), _lib.ptr(xh), _lib.ptr(r), _lib.ptr(p), _lib.ptr(A), _lib.ptr(P),
               N, float(tol), int(k_max), _lib.ptr(hist), _lib.ptr(status), _lib.stream_ptr())
     end.record()
-    x = transform_full(spectrum, xh)
+    x = transform_full_from_padded(spectrum, xh) if padded else transform_full(spectrum, xh)
     st = status.cpu().numpy()
     its, conv, bk_it, bk_kind = (int(v) for v in st)
     if bk_kind:
@@ -145,7 +166,9 @@ def solve_control_full(y_design, cfg, spectrum, precond="kronecker", mode="spect
         raise ValueError("expected a SolverConfig")
     if tuple(y_design.shape) != tuple(spectrum.mode_sizes):
         raise ValueError("design function dims do not match the spectrum")
-    A, P = cores if cores is not None else control_cores(cfg, spectrum, precond, seed)
+    if cores is None:
+        cores = control_cores(cfg, spectrum, precond, seed, layout="padded" if mode == "spectral" else "dense")
+    A, P = cores
     return pcg_full(spectrum, A, P, y_design, cfg.residual_tol, cfg.k_max, mode)
 
 
