@@ -329,8 +329,11 @@ int launch_reg10(DstArgs a, cudaStream_t st) {
     a.div_chunk = make_fastdiv((uint32_t)a.nchunks);
     if (!reg_tensor_map(a, &map) || !reg_out_maps(a, &om, 32)) return 0;
   }
-  auto kern = rg10::k_dst_reg10<SIN>;
-  constexpr size_t SMEM = rg10::smem_bytes();
+  constexpr int NW = SIN == rg::SIDE_CONTIG ? rg10::CONTIG_NW : 8;
+  constexpr int PIECES = 8 / NW;
+  if (a.ntiles * PIECES >= (int64_t(1) << 31)) return 0;
+  auto kern = rg10::k_dst_reg10<SIN, NW>;
+  constexpr size_t SMEM = rg10::smem_bytes<NW>();
   static std::atomic<uint64_t> attr_set{0};
   int dev = 0;
   FL_CUDA_TRY(cudaGetDevice(&dev));
@@ -339,9 +342,9 @@ int launch_reg10(DstArgs a, cudaStream_t st) {
     FL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
     attr_set.fetch_or(bit);
   }
-  const int64_t cap = (int64_t)sm_count();
-  const int grid = (int)(a.ntiles < cap ? a.ntiles : cap);
-  kern<<<grid, 32 * rg10::NWARP, SMEM, st>>>(a, map, om);
+  const int64_t cap = (int64_t)sm_count() * PIECES, pieces = a.ntiles * PIECES;
+  const int grid = (int)(pieces < cap ? pieces : cap);
+  kern<<<grid, 32 * NW, SMEM, st>>>(a, map, om);
   FL_LAUNCH_CHECK();
   return 1;
 }

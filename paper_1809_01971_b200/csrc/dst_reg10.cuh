@@ -208,23 +208,25 @@ __device__ __forceinline__ bool contig_bulk10(const DstArgs& a, const Tile& tl, 
 }
 
 // warp w's 2 lines: one bulk copy, or cp.async with per-line shift / zero fill
-__device__ __forceinline__ void issue_contig(const DstArgs& a, uint32_t t, double2* tile, uint32_t stile, int w,
-                                             int lane, uint64_t* wbar) {
+// (wl: the warp's smem slot, wg: its line pair 2 wg, 2 wg + 1 in the 16-line tile)
+__device__ __forceinline__ void issue_contig(const DstArgs& a, uint32_t t, double2* tile, uint32_t stile, int wl,
+                                             int wg, int lane, uint64_t* wbar) {
   const Tile tl = rg::tile_of<SIDE_CONTIG, false>(a, t);
-  if (contig_bulk10(a, tl, w)) {
+  if ((FL_REG_NOMEM == 1 || FL_REG_NOMEM == 2)) return;
+  if (contig_bulk10(a, tl, wg)) {
     if (lane == 0) {
       const uint32_t bytes = (uint32_t)(2 * tl.LS * sizeof(double));
       mbar_expect_tx(wbar, bytes);
-      rg::bulk_load(tile + 1024 * w, a.x + tl.base + (int64_t)(2 * w) * tl.LS, bytes, wbar);
+      rg::bulk_load(tile + 1024 * wl, a.x + tl.base + (int64_t)(2 * wg) * tl.LS, bytes, wbar);
     }
     return;
   }
-  const uint32_t d = stile + 8u * (uint32_t)(w * 2048) + 16u * (uint32_t)lane;
+  const uint32_t d = stile + 8u * (uint32_t)(wl * 2048) + 16u * (uint32_t)lane;
   rg::static_for<0, 2>([&](auto L) {
     constexpr int l = decltype(L)::value;
-    const bool ok = 2 * w + l < tl.lmax;
-    const int sh = ok ? rg::line_shift(tl, 2 * w + l) : 0;
-    const double* src = ok ? a.x + tl.base + (int64_t)(2 * w + l) * tl.LS - sh + 2 * lane : a.x;
+    const bool ok = 2 * wg + l < tl.lmax;
+    const int sh = ok ? rg::line_shift(tl, 2 * wg + l) : 0;
+    const double* src = ok ? a.x + tl.base + (int64_t)(2 * wg + l) * tl.LS - sh + 2 * lane : a.x;
     const int sz = ok ? 16 : 0;
     const int szl = ok ? (sh ? 16 : (lane == 31 ? 8 : 16)) : 0;
     rg::static_for<0, 16>([&](auto I) {
@@ -270,7 +272,7 @@ __device__ __forceinline__ void store_strided_tma(const DstArgs& a, const rg::Ou
     if (q >= 1 && ((q - 1) >> 4) == hh) stg[stg_idx(hh, q - 1, 31, ch)] = ev[0];
     rg::proxy_fence_async();
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && !(FL_REG_NOMEM == 1 || FL_REG_NOMEM == 3)) {
       if (hh == 0) {
         rg::tma_store_5d(&maps->a, stg, c0, 0, 0, (int)g, (int)o);
       } else {
@@ -278,9 +280,11 @@ __device__ __forceinline__ void store_strided_tma(const DstArgs& a, const rg::Ou
         rg::tma_store_5d(&maps->c, stg + 3840, c0, 31, 0, (int)g, (int)o);
       }
       rg::bulk_commit();
-      rg::bulk_wait_read();
+      if (hh == 0) rg::bulk_wait_read();
     }
-    __syncthreads();
+    // half 1's staging is reread by the TMA engine while the next tile is
+    // pre-read; the kernel waits for it before the next exchange
+    if (hh == 0) __syncthreads();
   }
 }
 
@@ -314,7 +318,7 @@ __device__ __forceinline__ void store_contig(const DstArgs& a, uint32_t t, doubl
     __syncwarp();
 #pragma unroll
     for (int l = 0; l < 2; ++l) {
-      if (2 * w + l < tl.lmax) {
+      if (2 * w + l < tl.lmax && (!(FL_REG_NOMEM == 1 || FL_REG_NOMEM == 3) || a.scale == 12345.0)) {
         const int64_t off = tl.base + (int64_t)(2 * w + l) * tl.LS + 512 * hh;
         const bool al = ((off & 1) == 0) && ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0);
         double* y = a.y + off;
@@ -337,19 +341,24 @@ __device__ __forceinline__ void store_contig(const DstArgs& a, uint32_t t, doubl
   }
 }
 
-// Persistent CTAs of 8 warps (one 16-line tile at a time), one per SM.
-template <int SIDE_IN>
-__global__ void __launch_bounds__(32 * NWARP, 1) k_dst_reg10(const DstArgs a, const __grid_constant__ CUtensorMap map,
-                                                             const __grid_constant__ rg::OutMaps omaps) {
+// Persistent CTAs of NW warps.  Strided: NW = 8, one 16-line tile at a time,
+// one CTA per SM.  Contiguous: NW = 8 or 4; with 4, a CTA takes one half
+// (8 lines) of a 16-line tile at a time and two CTAs share an SM, so one's
+// stores overlap the other's FFTs.
+template <int SIDE_IN, int NW>
+__global__ void __launch_bounds__(32 * NW, 8 / NW) k_dst_reg10(const DstArgs a, const __grid_constant__ CUtensorMap map,
+                                                               const __grid_constant__ rg::OutMaps omaps) {
+  static_assert(NW == 8 || (NW == 4 && SIDE_IN == SIDE_CONTIG), "strided tiles need 8 warps");
+  constexpr uint32_t PIECES = 8 / NW;  // CTA pieces per 16-line tile
   extern __shared__ __align__(1024) double2 smem10[];
   double2* const tile = smem10;
-  double2* const scr_all = smem10 + TILE;
-  uint64_t* const bar = reinterpret_cast<uint64_t*>(scr_all + NWARP * SCR);
+  double2* const scr_all = smem10 + NW * 1024;
+  uint64_t* const bar = reinterpret_cast<uint64_t*>(scr_all + NW * SCR);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint64_t* const wbar = bar + 1 + w;
   double2* const scr = scr_all + SCR * w;
   const uint32_t stile = rg::smem_u32(tile);
-  const uint32_t ntiles = (uint32_t)a.ntiles;
+  const uint32_t ntiles = (uint32_t)a.ntiles * PIECES;
   constexpr bool STRIDED = SIDE_IN != SIDE_CONTIG;
   if (STRIDED && (stile & 1023u) != 0) __trap();
   if (threadIdx.x == 0) mbar_init(bar, 1);
@@ -360,9 +369,9 @@ __global__ void __launch_bounds__(32 * NWARP, 1) k_dst_reg10(const DstArgs a, co
   uint32_t t = blockIdx.x;
   auto issue_next = [&](uint32_t tt) {
     if constexpr (STRIDED) {
-      if (threadIdx.x == 0) tma_issue(a, &map, tt, tile, bar);
+      if (threadIdx.x == 0 && !(FL_REG_NOMEM == 1 || FL_REG_NOMEM == 2)) tma_issue(a, &map, tt, tile, bar);
     } else {
-      issue_contig(a, tt, tile, stile, w, lane, wbar);
+      issue_contig(a, tt / PIECES, tile, stile, w, w + NW * (int)(tt % PIECES), lane, wbar);
     }
   };
   if (t < ntiles) issue_next(t);
@@ -370,18 +379,20 @@ __global__ void __launch_bounds__(32 * NWARP, 1) k_dst_reg10(const DstArgs a, co
   for (; t < ntiles; t += gridDim.x) {
     const uint32_t tn = t + gridDim.x;
     int sha = 0, shb = 0, sp = 1024;
+    const uint32_t tt = t / PIECES;                 // 16-line tile
+    const int wg = w + NW * (int)(t % PIECES);      // line pair in it
     if constexpr (STRIDED) {
-      mbar_wait(bar, phase);
+      if (!(FL_REG_NOMEM == 1 || FL_REG_NOMEM == 2)) mbar_wait(bar, phase);
       phase ^= 1;
     } else {
-      const Tile tin = rg::tile_of<SIDE_CONTIG, false>(a, t);
-      if (contig_bulk10(a, tin, w)) {
-        mbar_wait(wbar, wphase);
+      const Tile tin = rg::tile_of<SIDE_CONTIG, false>(a, tt);
+      if (contig_bulk10(a, tin, wg)) {
+        if (!(FL_REG_NOMEM == 1 || FL_REG_NOMEM == 2)) mbar_wait(wbar, wphase);
         wphase ^= 1;
         sp = (int)tin.LS;
       } else {
-        sha = rg::line_shift(tin, 2 * w);
-        shb = rg::line_shift(tin, 2 * w + 1);
+        sha = rg::line_shift(tin, 2 * wg);
+        shb = rg::line_shift(tin, 2 * wg + 1);
       }
     }
     rg::cp_wait<0>();
@@ -390,6 +401,7 @@ __global__ void __launch_bounds__(32 * NWARP, 1) k_dst_reg10(const DstArgs a, co
     const Lane c = lane_consts(a, lane);
     pre_read<!STRIDED>(tile, w, c, v, 0.5 * a.scale, sha, shb, sp);
     rg::proxy_fence_async();
+    if (STRIDED && threadIdx.x == 0) rg::bulk_wait_read();  // previous tile's half-1 store
     if (STRIDED) __syncthreads(); else __syncwarp();
     if (tn < ntiles) issue_next(tn);
     rg::cp_commit();
@@ -397,14 +409,20 @@ __global__ void __launch_bounds__(32 * NWARP, 1) k_dst_reg10(const DstArgs a, co
     if constexpr (STRIDED) {
       store_strided_tma(a, &omaps, t, scr_all, w, lane, ev, od);
     } else {
-      store_contig(a, t, scr, w, lane, ev, od);
+      store_contig(a, tt, scr, wg, lane, ev, od);
     }
   }
   rg::cp_wait<0>();
   if (STRIDED && threadIdx.x == 0) rg::bulk_wait_all();
 }
 
-constexpr size_t smem_bytes() { return (size_t)(TILE + NWARP * SCR + 8) * sizeof(double2); }
+template <int NW>
+constexpr size_t smem_bytes() { return (size_t)(NW * 1024 + NW * SCR + 8) * sizeof(double2); }
+
+#ifndef FL_R10_CNW
+#define FL_R10_CNW 8
+#endif
+constexpr int CONTIG_NW = FL_R10_CNW;
 
 }  // namespace rg10
 }  // namespace fl
