@@ -344,3 +344,43 @@ def test_apply_full_padded_n1023():
     x = np.random.default_rng(1023).standard_normal(dims)
     got = op(torch.tensor(x, device="cuda")).cpu().numpy()
     assert rel(got, oracle.apply_full(core, x)) <= 1e-12
+
+
+@pytest.mark.parametrize("lines,pin,pout", [(1, 1023, 1024), (17, 1023, 1023), (33, 1024, 1027), (100, 1027, 1024),
+                                            (16, 1024, 1024)])
+def test_dst1_pass_n1023_contiguous(lines, pin, pout):
+    """n = 1023 contiguous passes through the N = 1024 register kernel: dense
+    (1023), padded (1024) and odd (1027) pitches, ragged line counts (bulk
+    copies for whole line pairs, cp.async with shifts and zero fill
+    otherwise); the padding of the output stays untouched."""
+    from paper_1809_01971_b200 import _lib
+    n = 1023
+    rng = np.random.default_rng(lines + pin + pout)
+    x = rng.standard_normal((lines, pin))
+    want = oracle.dst(x[:, :n], axis=1)
+    xt = torch.tensor(x, device="cuda")
+    yt = torch.full((lines, pout), 7.0, dtype=torch.float64, device="cuda")
+    full.run_pass((_lib.ptr(xt), _lib.ptr(yt), None, n, 1, lines, 1, 1, (0, 1, 0, pin), (0, 1, 0, pout), 0.5))
+    got = yt.cpu().numpy()
+    assert rel(got[:, :n], 0.5 * want) <= 1e-13
+    assert np.all(got[:, n:] == 7.0)
+
+
+def test_transform_full_padded_n1023_deterministic():
+    """The padded n = 1023 transform (contiguous pass, then two TMA-stored
+    strided passes whose store drain overlaps the next tile) repeats bit for
+    bit, and matches the dense-layout transform."""
+    n = 1023
+    dims = (n, 7, n)
+    spec = spectral.EigenSpectrum(tuple(spectral.laplacian_mode(m) for m in dims))
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    x = torch.randn(dims, dtype=torch.float64, device="cuda", generator=g)
+    ref = full.transform_full_padded(spec, x).clone()
+    for _ in range(5):
+        assert torch.equal(full.transform_full_padded(spec, x), ref)
+    assert torch.all(ref[..., n:] == 0)
+    dense = full.transform_full(spec, x)
+    assert rel(ref[..., :n].cpu().numpy(), dense.cpu().numpy()) <= 1e-13
+    back = full.transform_full_from_padded(spec, ref.clone())
+    assert rel(back.cpu().numpy(), x.cpu().numpy()) <= 1e-13
