@@ -186,7 +186,9 @@ int fl_cp_gram(int d, const int64_t* n, const double* const* A, int64_t Ra,
  * matrix): A is batch x m x n row-major; U (batch, m, k), S (batch, k)
  * descending, Vt (batch, k, n), k = min(m, n).  The slice SVDs of t2c
  * (decomp.py:468-519).  Working set in shared memory up to m = n = 110,
- * beyond that in a device scratch allocated on the stream. */
+ * beyond that in a device scratch allocated on the stream.  Vt may be NULL
+ * when m >= n: left vectors and values only (no right rotations are
+ * accumulated), e.g. the square R factors of _left_sv. */
 int fl_svd_batched(const double* A, int batch, int m, int n, double* U, double* S,
                    double* Vt, void* stream);
 

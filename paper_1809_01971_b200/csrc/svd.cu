@@ -43,7 +43,8 @@ __device__ __forceinline__ void rr_pair(int N, int r, int k, int& p, int& q) {
 // Outputs: U (batch, m, k), S (batch, k), Vt (batch, k, n), k = min(m, n).
 // Placement: W and V in shared memory when both fit, else V (and if need be
 // W) in a global scratch buffer (scratch != nullptr; per matrix M*K + K*K
-// doubles), which stays L2-resident for the sizes of t2c.
+// doubles), which stays L2-resident for the sizes of t2c.  Vt == nullptr
+// (m >= n only): left vectors and values only, no V is accumulated.
 __global__ void __launch_bounds__(SVD_THREADS) k_svd_jacobi(const double* __restrict__ A, int m, int n,
                                                             double* __restrict__ U, double* __restrict__ S,
                                                             double* __restrict__ Vt, int max_sweeps,
@@ -53,12 +54,13 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd_jacobi(const double* __rest
   const int M = tr ? n : m;  // rows of the working matrix W
   const int K = tr ? m : n;  // columns of W (= number of singular values)
   const int N = K + (K & 1);
+  const bool want_v = Vt != nullptr;
   double* gs = scratch ? scratch + (size_t)blockIdx.x * ((size_t)M * K + (size_t)K * K) : nullptr;
   double* sp = sm_svd;
   double* W = w_in_smem ? sp : gs;  // column-major M x K
   if (w_in_smem) sp += (size_t)M * K;
-  double* V = v_in_smem ? sp : gs + (size_t)M * K;  // column-major K x K
-  if (v_in_smem) sp += (size_t)K * K;
+  double* V = !want_v ? nullptr : v_in_smem ? sp : gs + (size_t)M * K;  // column-major K x K
+  if (want_v && v_in_smem) sp += (size_t)K * K;
   int* flag = reinterpret_cast<int*>(sp);
   const double* Ab = A + (size_t)blockIdx.x * m * n;
   // load W = A (columns of A) or A^T (rows of A) column-major
@@ -69,7 +71,8 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd_jacobi(const double* __rest
     else
       W[(size_t)i * M + j] = Ab[idx];
   }
-  for (int idx = threadIdx.x; idx < K * K; idx += blockDim.x) V[idx] = (idx / K == idx % K) ? 1.0 : 0.0;
+  if (want_v)
+    for (int idx = threadIdx.x; idx < K * K; idx += blockDim.x) V[idx] = (idx / K == idx % K) ? 1.0 : 0.0;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const double tol = 1e-15 * (double)M;
@@ -103,6 +106,7 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd_jacobi(const double* __rest
           wp[i] = c * x - s * y;
           wq[i] = s * x + c * y;
         }
+        if (!want_v) continue;
         double* vp = V + (size_t)p * K;
         double* vq = V + (size_t)q * K;
         for (int i = lane; i < K; i += 32) {
@@ -129,7 +133,7 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd_jacobi(const double* __rest
   __syncthreads();
   double* Ub = U + (size_t)blockIdx.x * m * K;
   double* Sb = S + (size_t)blockIdx.x * K;
-  double* Vb = Vt + (size_t)blockIdx.x * K * n;
+  double* Vb = want_v ? Vt + (size_t)blockIdx.x * K * n : nullptr;
   for (int j = warp; j < K; j += nwarps) {
     const double sj = sig[j];
     int rank = 0;
@@ -139,11 +143,12 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd_jacobi(const double* __rest
     if (lane == 0) Sb[rank] = sj;
     const double inv = sj > 0.0 ? 1.0 / sj : 0.0;
     const double* wj = W + (size_t)j * M;
-    const double* vj = V + (size_t)j * K;
+    const double* vj = want_v ? V + (size_t)j * K : nullptr;
     if (!tr) {
       // A = W_final V^T: U[:, rank] = w_j / s_j (m rows), Vt[rank, :] = v_j (n = K)
       for (int i = lane; i < m; i += 32) Ub[(size_t)i * K + rank] = (sj > 0.0) ? wj[i] * inv : (i == j ? 1.0 : 0.0);
-      for (int i = lane; i < n; i += 32) Vb[(size_t)rank * n + i] = vj[i];
+      if (want_v)
+        for (int i = lane; i < n; i += 32) Vb[(size_t)rank * n + i] = vj[i];
     } else {
       // A^T = W V^T -> A = V W^T: U[:, rank] = v_j (m = K rows), Vt[rank, :] = w_j / s_j
       for (int i = lane; i < m; i += 32) Ub[(size_t)i * K + rank] = vj[i];
@@ -158,8 +163,9 @@ constexpr size_t SVD_SMEM_CAP = 200 * 1024;
 
 int svd_batched(const double* A, int batch, int m, int n, double* U, double* S, double* Vt, cudaStream_t st) {
   FL_ARG_CHECK(batch >= 0 && m >= 1 && n >= 1, "bad batched SVD shape (%d, %d, %d)", batch, m, n);
+  FL_ARG_CHECK(Vt != nullptr || m >= n, "batched SVD without Vt needs m >= n, got %d x %d", m, n);
   const size_t M = m > n ? m : n, K = m < n ? m : n;
-  const size_t wb = sizeof(double) * M * K, vb = sizeof(double) * K * K, tail = sizeof(double) * K + 2 * sizeof(int);
+  const size_t wb = sizeof(double) * M * K, vb = Vt ? sizeof(double) * K * K : 0, tail = sizeof(double) * K + 2 * sizeof(int);
   FL_ARG_CHECK(tail <= SVD_SMEM_CAP, "batched SVD: %d x %d matrices are too large", m, n);
   if (batch == 0) return FL_OK;
   int w_sm = 0, v_sm = 0;

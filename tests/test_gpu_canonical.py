@@ -254,6 +254,20 @@ def test_svd_batched_matches_numpy(b, m, n):
         assert np.allclose(Vk @ Vk.T, np.eye(keep.sum()), atol=1e-12)
 
 
+@pytest.mark.parametrize("b,m,n", [(4, 40, 17), (2, 64, 64), (3, 140, 130)])
+def test_svd_batched_left_only(b, m, n):
+    """Vt = NULL (m >= n): the same rotations without the right factor, so U
+    and S are bit-identical to the full call; m < n is rejected."""
+    from paper_1809_01971_b200.decomp import svd_batched
+    A = torch.tensor(np.random.default_rng(b * m + n).standard_normal((b, m, n)), device="cuda")
+    U, S, Vt = svd_batched(A)
+    U1, S1, V1 = svd_batched(A, right=False)
+    assert V1 is None and torch.equal(U1, U) and torch.equal(S1, S)
+    if m > n:
+        with pytest.raises(ValueError):
+            svd_batched(A.transpose(1, 2), right=False)
+
+
 def test_apply_compressed_matches_apply_then_trunc(monkeypatch):
     """trunc(apply_compressed(op, x)) == trunc(apply(op, x)): same kept rank,
     same tensor far below the truncation tolerance (compression forced on a
