@@ -370,6 +370,7 @@ def run_solves(args, rank, world, dev):
         spec = fl.laplacian_spectrum(n, 3)
         y = fl.gaussian_bumps(n, 3, 8, seed=11)
         cfg = fl.SolverConfig(alpha=0.5, beta=1e-2, eps=1e-8, precond_rank=6, residual_tol=1e-6, k_max=60)
+        fl.solve_control(y, cfg, spec)  # warm-up (cuSOLVER handles, kernel loads, allocator)
         (u, rep), t = _dev_time(lambda: fl.solve_control(y, cfg, spec), 1)
         out["config1_3d_canonical"] = {"n": n, "alpha": 0.5, "seconds": t, "iterations": rep.iterations,
                                        "final_rank": u.rank, "final_residual": rep.residuals[-1],
@@ -396,15 +397,26 @@ def run_solves(args, rank, world, dev):
             A, P = full.to_padded(A), full.to_padded(P)
         return A, P
 
-    (A, P), t_setup = _dev_time(setup, world)
     ops = D.CudaOps()
+
+    def solve(A, P):
+        if world == 1:
+            return fullsolve.solve_control_full(y, cfg, spec, cores=(A, P))
+        return D.pcg_slab(y, A, P, lay, ops, cfg.residual_tol, cfg.k_max)
+
+    # one untimed setup + solve first: the timed pair then measures the
+    # solver, not first-launch module loads and the caching allocator's
+    # first multi-GB cudaMallocs
+    warm = setup()
+    solve(*warm)
+    del warm
+    (A, P), t_setup = _dev_time(setup, world)
     if world == 1:
-        (u, rep), t_solve = _dev_time(lambda: fullsolve.solve_control_full(y, cfg, spec, cores=(A, P)), 1)
+        (u, rep), t_solve = _dev_time(lambda: solve(A, P), 1)
         its, res = rep.iterations, rep.residuals[-1]
         path = "spectral PCG, 1 persistent kernel (padded spectral layout)"
     else:
-        (u, its, hist, conv), t_solve = _dev_time(lambda: D.pcg_slab(y, A, P, lay, ops, cfg.residual_tol, cfg.k_max),
-                                                   world)
+        (u, its, hist, conv), t_solve = _dev_time(lambda: solve(A, P), world)
         res = hist[-1]
         path = "slab-partitioned: NCCL all_to_all transposes + phase kernels with scalar all-reduces"
     out["config3_3d_slab"] = {"n": n, "n_gpus": world, "setup_s": t_setup, "solve_s": t_solve, "iterations": its,
