@@ -104,19 +104,25 @@ __device__ __forceinline__ void pre_read(const double2* tile, int w, const Lane&
   }
 }
 
-// FFT, split and scan of lane q's FFT; ev[i] = S'_{2k}, od[i] = S'_{2k+1},
-// k = 16q + i (scaled: the pass's scale rode on the pre-processing)
-__device__ __forceinline__ void fft_split(double2* sf, const Lane& c, double2 (&v)[32], double2 (&ev)[16],
-                                          double2 (&od)[16]) {
-  const int q = c.q, q7 = q & 7;
+#ifndef FL_R10_XTILE
+#define FL_R10_XTILE 1
+#endif
+
+// First half of lane q's FFT: 32-point DFTs, twiddles, the transpose and the
+// second 32-point DFTs; w[i] = X[q + 32 brev(i)].  XTILE: the transpose runs
+// in one round through a 16 KB buffer xb (the warp's slice of the consumed
+// input tile), so a lane never holds more than its 32 values; otherwise two
+// rounds through the 8 KB scratch sf (readers then hold 16 unwritten values
+// plus 32 received, which spills).
+template <bool XTILE>
+__device__ __forceinline__ void fft_a(double2* xb, double2* sf, const Lane& c, double2 (&v)[32],
+                                      double2 (&w)[32]) {
+  const int q = c.q;
   rg::dif<32>(v);
-  double2 w[32];
-  // exchange in two rounds of k2: entry (kk, q') at kk * 32 + (q' ^ (kk & 7))
+  if constexpr (XTILE) {
+    // entry (k2, q') at k2 * 32 + (q' ^ (k2 & 7))
 #pragma unroll
-  for (int rd = 0; rd < 2; ++rd) {
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      const int h = 2 * rd + hh;
+    for (int h = 0; h < 4; ++h) {
       double2 t = h == 1 ? c.w8 : h == 2 ? c.w16 : c.w24;
 #pragma unroll
       for (int l = 0; l < 8; ++l) {
@@ -125,19 +131,49 @@ __device__ __forceinline__ void fft_split(double2* sf, const Lane& c, double2 (&
         if (h == 0 && l == 1) t = c.w1;
         if ((h == 0 && l >= 2) || (h > 0 && l >= 1)) t = cmul(t, c.w1);
         if (k2) val = cmul(val, t);
-        const int kk = k2 & 15;
-        sf[kk * 32 + (q ^ (kk & 7))] = val;
+        xb[k2 * 32 + (q ^ (k2 & 7))] = val;
       }
     }
     __syncwarp();
-    if ((q >> 4) == rd) {
-      const int kk = q & 15;
 #pragma unroll
-      for (int qq = 0; qq < 32; ++qq) w[qq] = sf[kk * 32 + (qq ^ (kk & 7))];
+    for (int qq = 0; qq < 32; ++qq) w[qq] = xb[q * 32 + (qq ^ (q & 7))];
+  } else {
+    // two rounds of k2: entry (kk, q') at kk * 32 + (q' ^ (kk & 7))
+#pragma unroll
+    for (int rd = 0; rd < 2; ++rd) {
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int h = 2 * rd + hh;
+        double2 t = h == 1 ? c.w8 : h == 2 ? c.w16 : c.w24;
+#pragma unroll
+        for (int l = 0; l < 8; ++l) {
+          const int k2 = 8 * h + l;
+          double2 val = v[brev(k2, 5)];
+          if (h == 0 && l == 1) t = c.w1;
+          if ((h == 0 && l >= 2) || (h > 0 && l >= 1)) t = cmul(t, c.w1);
+          if (k2) val = cmul(val, t);
+          const int kk = k2 & 15;
+          sf[kk * 32 + (q ^ (kk & 7))] = val;
+        }
+      }
+      __syncwarp();
+      if ((q >> 4) == rd) {
+        const int kk = q & 15;
+#pragma unroll
+        for (int qq = 0; qq < 32; ++qq) w[qq] = sf[kk * 32 + (qq ^ (kk & 7))];
+      }
+      __syncwarp();
     }
-    __syncwarp();
   }
   rg::dif<32>(w);  // w[i] = X[q + 32 brev(i)]
+}
+
+// Second half: spectrum staging, split and scan; ev[i] = S'_{2k},
+// od[i] = S'_{2k+1}, k = 16q + i (scaled: the pass's scale rode on the
+// pre-processing)
+__device__ __forceinline__ void fft_b(double2* sf, const Lane& c, double2 (&w)[32], double2 (&ev)[16],
+                                      double2 (&od)[16]) {
+  const int q = c.q, q7 = q & 7;
   // spectrum staging in two rounds (k < 512, k >= 512): kk = k mod 512 at
   // kk ^ ((kk >> 4) & 7)
   double2 ck[16], cm[16];
@@ -397,15 +433,28 @@ __global__ void __launch_bounds__(32 * NW, 8 / NW) k_dst_reg10(const DstArgs a, 
     }
     rg::cp_wait<0>();
     if (STRIDED) __syncthreads(); else __syncwarp();
-    double2 v[32], ev[16], od[16];
+    double2 v[32], wv[32], ev[16], od[16];
     const Lane c = lane_consts(a, lane);
     pre_read<!STRIDED>(tile, w, c, v, 0.5 * a.scale, sha, shb, sp);
-    rg::proxy_fence_async();
-    if (STRIDED && threadIdx.x == 0) rg::bulk_wait_read();  // previous tile's half-1 store
-    if (STRIDED) __syncthreads(); else __syncwarp();
-    if (tn < ntiles) issue_next(tn);
-    rg::cp_commit();
-    fft_split(scr, c, v, ev, od);
+    if constexpr (FL_R10_XTILE) {
+      // the tile is consumed: warp w's 16 KB slice of it carries the
+      // transpose, then the next tile is issued into it
+      if (STRIDED) __syncthreads(); else __syncwarp();
+      fft_a<true>(tile + 1024 * w, scr, c, v, wv);
+      rg::proxy_fence_async();
+      if (STRIDED && threadIdx.x == 0) rg::bulk_wait_read();  // previous tile's half-1 store
+      if (STRIDED) __syncthreads(); else __syncwarp();
+      if (tn < ntiles) issue_next(tn);
+      rg::cp_commit();
+    } else {
+      rg::proxy_fence_async();
+      if (STRIDED && threadIdx.x == 0) rg::bulk_wait_read();  // previous tile's half-1 store
+      if (STRIDED) __syncthreads(); else __syncwarp();
+      if (tn < ntiles) issue_next(tn);
+      rg::cp_commit();
+      fft_a<false>(nullptr, scr, c, v, wv);
+    }
+    fft_b(scr, c, wv, ev, od);
     if constexpr (STRIDED) {
       store_strided_tma(a, &omaps, t, scr_all, w, lane, ev, od);
     } else {
