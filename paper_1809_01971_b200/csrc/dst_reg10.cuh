@@ -469,7 +469,7 @@ template <int NW>
 constexpr size_t smem_bytes() { return (size_t)(NW * 1024 + NW * SCR + 8) * sizeof(double2); }
 
 #ifndef FL_R10_CNW
-#define FL_R10_CNW 8
+#define FL_R10_CNW 4
 #endif
 constexpr int CONTIG_NW = FL_R10_CNW;
 
