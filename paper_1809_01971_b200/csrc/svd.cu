@@ -29,7 +29,11 @@ __device__ __forceinline__ double warp_sum(double v) {
 // players 0..N-1 (N even): round r pairs 0 with pos(0) and pos(k) with
 // pos(N-1-k), pos(i) = 1 + (i + r) mod (N - 1)
 __device__ __forceinline__ void rr_pair(int N, int r, int k, int& p, int& q) {
-  auto pos = [&](int i) { return 1 + (i + r) % (N - 1); };
+  // i + r < 2 (N - 1): one conditional subtraction instead of a modulo
+  auto pos = [&](int i) {
+    const int x = i + r;
+    return 1 + (x >= N - 1 ? x - (N - 1) : x);
+  };
   if (k == 0) {
     p = 0;
     q = pos(0);
@@ -186,7 +190,10 @@ int svd_batched(const double* A, int batch, int m, int n, double* U, double* S, 
     FL_CUDA_TRY(cudaFuncSetAttribute(k_svd_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SVD_SMEM_CAP));
     attr_set.fetch_or(bit);
   }
-  k_svd_jacobi<<<batch, SVD_THREADS, smem, st>>>(A, m, n, U, S, Vt, 40, scratch, w_sm, v_sm);
+#ifndef FL_SVD_SWEEPS
+#define FL_SVD_SWEEPS 40
+#endif
+  k_svd_jacobi<<<batch, SVD_THREADS, smem, st>>>(A, m, n, U, S, Vt, FL_SVD_SWEEPS, scratch, w_sm, v_sm);
   FL_LAUNCH_CHECK();
   if (scratch) FL_CUDA_TRY(cudaFreeAsync(scratch, st));
   return FL_OK;

@@ -22,7 +22,7 @@ os.makedirs(odir, exist_ok=True)
 objs = []
 for src in B.sources():
     base = os.path.basename(src).replace(".cu", ".o")
-    if base == "dst.o":
+    if base == os.environ.get("VARIANT_OBJ", "dst.o"):
         obj = os.path.join(odir, base)
         cmd = [B._nvcc()] + B.ARCH + B.NVCC_FLAGS + flags + ["-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
