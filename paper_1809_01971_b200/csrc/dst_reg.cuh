@@ -823,7 +823,11 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
       }
     }
     cp_wait<0>();
-    if (STRIDED) __syncthreads(); else __syncwarp();
+    // TMA tiles: every thread waited on the tile's mbarrier itself, which
+    // makes the bytes visible to it; only cooperative cp.async tiles need the
+    // CTA barrier
+    if constexpr (STRIDED && !TMA) __syncthreads();
+    if constexpr (!STRIDED) __syncwarp();
     double2 v[32], ev[16], od[16];
     if constexpr (!MID) {
       const Lane c = lane_consts(a, lane);

@@ -432,7 +432,8 @@ __global__ void __launch_bounds__(32 * NW, 8 / NW) k_dst_reg10(const DstArgs a, 
       }
     }
     rg::cp_wait<0>();
-    if (STRIDED) __syncthreads(); else __syncwarp();
+    // strided tiles arrive by TMA and every thread waited on the mbarrier
+    if constexpr (!STRIDED) __syncwarp();
     double2 v[32], wv[32], ev[16], od[16];
     const Lane c = lane_consts(a, lane);
     pre_read<!STRIDED>(tile, w, c, v, 0.5 * a.scale, sha, shb, sp);
