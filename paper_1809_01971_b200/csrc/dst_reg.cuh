@@ -700,6 +700,9 @@ __device__ __forceinline__ int stg_tma_idx(int hh, int qq, int ii, int ch) {
   return 1792 + ii * 8 + (ch ^ (ii & 7));
 }
 
+// DEFER: half 1's staging is drained by the kernel before the next exchange
+// instead of here (measured: helps the fused pass, costs the plain one)
+template <bool DEFER>
 __device__ __forceinline__ void store_strided_tma(const DstArgs& a, const OutMaps* maps, uint32_t t, double2* stg,
                                                   int w, int f, int q, const double2 (&ev)[16],
                                                   const double2 (&od)[16]) {
@@ -731,9 +734,9 @@ __device__ __forceinline__ void store_strided_tma(const DstArgs& a, const OutMap
         tma_store_5d(&maps->c, stg + 1792, c0, 15, 0, (int)g, (int)o);
       }
       bulk_commit();
-      bulk_wait_read();
+      if (!DEFER || hh == 0) bulk_wait_read();
     }
-    __syncthreads();
+    if (!DEFER || hh == 0) __syncthreads();
   }
 }
 
@@ -859,6 +862,7 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
         // proxy (core slice / TMA / bulk refill): fence the generic-proxy
         // reads (and phase 1's z writes) first
         proxy_fence_async();
+        if (TST && ph == 0 && threadIdx.x == 0) bulk_wait_read();  // previous tile's half-1 store
         if (STRIDED) __syncthreads(); else __syncwarp();
         if (ph == 0) {
           // bring the unit's lane-ordered core slice into quarter w while the
@@ -905,7 +909,7 @@ __global__ void __launch_bounds__(32 * NWARP, 2) k_dst_grp(const DstArgs a, cons
     const double sc = 1.0;
     if constexpr (STRIDED) {
       if constexpr (TST) {
-        store_strided_tma(a, &omaps, t, scr_all, w, lane >> 4, lane & 15, ev, od);
+        store_strided_tma<MID>(a, &omaps, t, scr_all, w, lane >> 4, lane & 15, ev, od);
       } else {
         store_strided<SIDE_OUT>(a, t, scr_all, w, lane, lane >> 4, lane & 15, ev, od, sc);
       }
