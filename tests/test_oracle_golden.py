@@ -119,3 +119,22 @@ def test_pcg_dense_oracle_on_config0_operator():
     assert ok
     assert abs(it - int(g["iters"])) <= 1
     assert rel(x, oracle.cp_to_dense(uw, uf)) <= 1e-8
+
+
+@pytest.mark.parametrize("n3", [15, 31])
+def test_kkt_oracle_matches_reference_3d_control_solves(n3):
+    """The oracle's exact spectral optimality solve reproduces the reference's
+    truncated 3D control solves (solver.py:203-216, residual_tol 1e-6, eps 1e-8)
+    to within the reference's own PCG tolerance, and the oracle's dense PCG
+    (identity preconditioner) agrees with both."""
+    g = load("solve")
+    key = "c3_n%d" % n3
+    y = oracle.cp_to_dense(g[key + "_y_w"], [g[key + "_y_f%d" % i] for i in range(3)])
+    alpha, beta, gamma = float(g[key + "_alpha"]), 1e-2, 1.0
+    _, u = oracle.kkt_dense_solve(y, alpha, beta, gamma)
+    assert rel(u, g[key + "_u"]) <= 1e-6
+    lam = oracle.laplacian_eigenvalues(n3)
+    A = oracle.dense_core("g2", [lam] * 3, alpha, beta, gamma / beta)
+    x, _, _, ok = oracle.pcg_dense(lambda v: oracle.apply_full(A, v), lambda v: v, y, 1e-6, 200)
+    assert ok
+    assert rel(x, u) <= 1e-5
