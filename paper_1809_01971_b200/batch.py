@@ -121,14 +121,30 @@ def solve_control_large(y_design, cfg, spectrum, max_level=1023):
     return pcg(fun, pre, y_design, None, cfg)
 
 
+def problem_params(i, seed=2026):
+    """(alpha, beta, target seed) of problem i: alpha ~ U(0.1, 0.9), beta
+    log-uniform in [1e-5, 1e-1]; a function of (seed, i) only, so every rank
+    count draws the same batch."""
+    rng = np.random.default_rng([seed, i])
+    alpha = float(rng.uniform(0.1, 0.9))
+    beta = float(10.0 ** rng.uniform(-5.0, -1.0))
+    return alpha, beta, seed * 1000 + i
+
+
+def problem_indices(count, rank=0, world=1):
+    """Problems owned by `rank`: round-robin, disjoint and covering over ranks
+    (no collective on the data path)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("rank %r outside world %r" % (rank, world))
+    return list(range(rank, count, world))
+
+
 def problem(i, n, seed=2026):
     """Problem i of the configs[4] batch: alpha ~ U(0.1, 0.9), beta log-uniform in
     [1e-5, 1e-1], rank-16 Gaussian-bump target (seeded per problem)."""
     from .rhs import gaussian_bumps
-    rng = np.random.default_rng([seed, i])
-    alpha = float(rng.uniform(0.1, 0.9))
-    beta = float(10.0 ** rng.uniform(-5.0, -1.0))
-    y = gaussian_bumps(n, 3, 16, seed=seed * 1000 + i)
+    alpha, beta, tseed = problem_params(i, seed)
+    y = gaussian_bumps(n, 3, 16, seed=tseed)
     cfg = SolverConfig(alpha=alpha, beta=beta, eps=1e-6, precond_rank=6, residual_tol=1e-6, k_max=60)
     return y, cfg
 
@@ -138,7 +154,7 @@ def solve_batch(n, count, rank=0, world=1, max_level=1023):
     from .spectral import laplacian_spectrum
     spec = laplacian_spectrum(n, 3)
     out = []
-    for i in range(rank, count, world):
+    for i in problem_indices(count, rank, world):
         y, cfg = problem(i, n)
         torch.cuda.synchronize()
         t0 = time.perf_counter()

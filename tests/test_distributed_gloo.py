@@ -114,3 +114,44 @@ def test_split_is_balanced_and_covering():
             assert all(b[i][1] == b[i + 1][0] for i in range(p - 1))
             sizes = [e - s for s, e in b]
             assert max(sizes) - min(sizes) <= 1
+
+
+def _batch_worker(rank, world, port, count, q):
+    from paper_1809_01971_b200 import batch
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mine = [(i,) + batch.problem_params(i) for i in batch.problem_indices(count, rank, world)]
+        got = [None] * world
+        dist.all_gather_object(got, mine)
+        q.put((rank, got))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,count", [(2, 64), (3, 7)])
+def test_batch_problems_spread_over_ranks(world, count):
+    """configs[4]: independent problems spread over ranks (batch.solve_batch)
+    with no data-path collective; the gathered assignment is a disjoint cover
+    of the batch and each problem's parameters do not depend on the rank count."""
+    from paper_1809_01971_b200 import batch
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batch_worker, args=(r, world, port, count, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = {i: batch.problem_params(i) for i in range(count)}
+    for _, got in res:
+        flat = [rec for part in got for rec in part]
+        assert sorted(r[0] for r in flat) == list(range(count))
+        for i, alpha, beta, tseed in flat:
+            assert (alpha, beta, tseed) == want[i]
+            assert 0.1 <= alpha <= 0.9 and 1e-5 <= beta <= 1e-1
+    with pytest.raises(ValueError):
+        batch.problem_indices(4, 2, 2)
