@@ -99,14 +99,23 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_apply_rate(n, workers):
-    """Oracle full-format apply on the host: returns (GDoF/s, seconds)."""
+def workload_config(n, world):
+    """The `config` dict of BOTH arms (GPU and --impl reference): same keys, same values."""
+    return {"workload": "BASELINE configs[2]: 3D full-format operator apply A^-alpha", "n": n, "alpha": ALPHA,
+            "dof_per_rank": n ** 3, "tensor_bytes": 8 * n ** 3,
+            "l2": "inputs (1.07 GB) larger than L2 (126 MB); no flush needed",
+            "parallelism": "replicas x%d" % world}
+
+
+def cpu_apply(x, workers):
+    """Oracle full-format apply A^-alpha x on the host (scipy DST-I per mode,
+    exactly the reference's spectral.dst_apply route, spectral.py:163-186):
+    returns (y, seconds)."""
     import numpy as np
     import oracle
-    rng = np.random.default_rng(7)
-    x = rng.standard_normal((n, n, n))
-    core = oracle.dense_core("g1", [oracle.laplacian_eigenvalues(n)] * 3, ALPHA)
     import scipy.fft
+    n = x.shape[0]
+    core = oracle.dense_core("g1", [oracle.laplacian_eigenvalues(n)] * 3, ALPHA)
     t0 = time.perf_counter()
     z = x
     for ax in range(3):
@@ -114,36 +123,66 @@ def cpu_apply_rate(n, workers):
     z *= core
     for ax in range(3):
         z = scipy.fft.dst(z, type=1, norm="ortho", axis=ax, workers=workers)
-    dt = time.perf_counter() - t0
+    return z, time.perf_counter() - t0
+
+
+def cpu_apply_rate(n, workers):
+    """Oracle full-format apply on a seeded N(0,1) n^3 tensor: returns (GDoF/s, seconds)."""
+    import numpy as np
+    x = np.random.default_rng(7).standard_normal((n, n, n))
+    _, dt = cpu_apply(x, workers)
     return n ** 3 / dt / 1e9, dt
+
+
+def cpu_config0_solve():
+    """BASELINE configs[0] on the host: the reference's 2D control solve
+    (solver.py:203-216) restated by the oracle in full format (rank-6 reciprocal
+    SVD preconditioner, fracop.py:392-402; dense PCG, solver.py:116-180).
+    Returns a dict with setup / solve / total seconds, like the GPU arm's."""
+    import numpy as np
+    import oracle
+    n, alpha, beta, gamma = 255, 0.5, 1e-3, 1.0
+    t0 = time.perf_counter()
+    lam = oracle.laplacian_eigenvalues(n)
+    A = oracle.dense_core("g2", [lam, lam], alpha, beta, gamma / beta)
+    P = oracle.reciprocal_svd_core("g2", [lam, lam], alpha, beta, gamma / beta, 6)
+    yw, yf = oracle.gaussian_bumps(n, 2, 4, seed=2024)
+    b = oracle.cp_to_dense(yw, yf)
+    t1 = time.perf_counter()
+    x, hist, it, ok = oracle.pcg_dense(lambda v: oracle.apply_full(A, v), lambda v: oracle.apply_full(P, v),
+                                       b, 1e-8, 100)
+    t2 = time.perf_counter()
+    return {"n": n, "setup_s": t1 - t0, "solve_s": t2 - t1, "seconds": t2 - t0, "iterations": it,
+            "final_residual": hist[-1], "converged": ok,
+            "path": "host: oracle dense PCG + rank-6 SVD preconditioner (numpy/scipy)"}
 
 
 def run_reference(args):
     rank, world, _ = _env_rank()
     if rank != 0:
         return 0
+    import numpy as np
     workers = os.cpu_count() or 1
-    # bounded sample: n=511 when K steps fit in ~150 s, else the n=255 cube
-    _, t255 = cpu_apply_rate(255, workers)
-    est511 = t255 * 8.5
-    n = 511 if est511 * (args.steps + args.warmup) <= 150.0 else 255
+    n = args.n
+    x = np.random.default_rng(7).standard_normal((n, n, n))
     for _ in range(args.warmup):
-        cpu_apply_rate(n, workers)
+        cpu_apply(x, workers)
     times = []
     for _ in range(args.steps):
-        times.append(cpu_apply_rate(n, workers)[1])
+        times.append(cpu_apply(x, workers)[1])
     total = sum(times)
     value = args.steps * n ** 3 / total / 1e9
-    sample = "one full A^-alpha apply per step on an n=%d cube (scipy DST-I, %d worker threads)" % (n, workers)
+    sample = "one full A^-alpha apply per step on the n=%d cube (scipy DST-I, %d worker threads)" % (n, workers)
+    solve0 = cpu_config0_solve()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic seeded N(0,1)",
-        "config": {"workload": "3D full-format operator apply A^-alpha", "n": n, "alpha": ALPHA,
-                   "parallelism": "host threads"},
+        "data": "synthetic seeded N(0,1) fp64 tensor per rank",
+        "config": workload_config(n, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "solves": {"config0_2d_full": solve0},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -267,11 +306,7 @@ def run_gpu(args):
 
     solves = None
     if not args.no_solves:
-        try:
-            solves = run_solves(args, rank, world, dev)
-        except Exception as exc:  # a solver failure must not cost the apply measurement
-            solves = {"error": "%s: %s" % (type(exc).__name__, str(exc)[:300])}
-            torch.cuda.empty_cache()
+        solves = run_solves(args, rank, world, dev)
 
     if rank == 0:
         peak, peak_kind = _peaks()
@@ -292,12 +327,9 @@ def run_gpu(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": 1e3 * t_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic seeded N(0,1) fp64 tensor per rank",
-            "config": {"workload": "BASELINE configs[2]: 3D full-format operator apply A^-alpha", "n": n,
-                       "alpha": ALPHA, "dof_per_rank": N3, "tensor_bytes": 8 * N3,
-                       "l2": "inputs (1.07 GB) larger than L2 (126 MB); no flush needed",
-                       "parallelism": "replicas x%d" % world,
-                       "layout": "x, y dense C order; internal work tensor and core with last-mode rows padded to %s doubles"
-                                 % (op.pitch if op.padded else "n (unpadded)")},
+            "config": workload_config(n, world),
+            "layout": "x, y dense C order; internal work tensor and core with last-mode rows padded to %s doubles"
+                      % (op.pitch if op.padded else "n (unpadded)"),
             "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": dbpe * N3, "avg_launch_ms": 1e3 * avg,
@@ -312,9 +344,23 @@ def run_gpu(args):
         if solves is not None:
             line["solves"] = solves
         if world == 1 and not args.no_cpu:
+            # CPU leg: the oracle applies A^-alpha to the SAME seeded tensor;
+            # its result is the parity check of the GPU apply at the exact
+            # configs[2] size (north_star: <= 1e-10 relative in fp64)
+            import numpy as np
             workers = os.cpu_count() or 1
             cpu_apply_rate(127, workers)
-            rate, dt = cpu_apply_rate(n, workers)
+            xh = x.cpu().numpy()
+            want, dt = cpu_apply(xh, workers)
+            rate = N3 / dt / 1e9
+            got = op(x).cpu().numpy()
+            diff = got - want
+            line["parity"] = {"vs": "oracle.apply_full (scipy DST-I per mode = reference spectral.py:163-186)",
+                              "rel_l2": float(np.linalg.norm(diff) / np.linalg.norm(want)),
+                              "max_rel": float(np.abs(diff).max() / np.abs(want).max()),
+                              "tolerance": 1e-10}
+            line["parity"]["ok"] = line["parity"]["rel_l2"] <= 1e-10 and line["parity"]["max_rel"] <= 1e-10
+            del got, diff, want, xh
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": workers, "kind": "port",
                                     "sample": "one A^-alpha apply on the n=%d cube (%.1f s, scipy DST-I)" % (n, dt)}
         print(json.dumps(line), flush=True)
@@ -344,12 +390,53 @@ def _dev_time(fn, world):
     return out, t
 
 
-def run_solves(args, rank, world, dev):
-    """PCG control solves of BASELINE configs[0], [1] (rank 0) and [3] (all ranks)."""
-    import numpy as np
+def _all_ok(ok, world, dev):
+    """Agree across ranks whether every rank's section succeeded (a failure on
+    one rank must not leave the others waiting in a later collective)."""
+    if world == 1:
+        return ok
     import torch
+    import torch.distributed as dist
+    t = torch.tensor([0 if ok else 1], dtype=torch.int32, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return int(t) == 0
+
+
+def run_solves(args, rank, world, dev):
+    """Solver sections (configs[0], [1] on rank 0; [3] and [4] on all ranks).
+    Each section is guarded: an exception is recorded in the JSON line, the
+    ranks agree on it before the next collective section, and the apply
+    measurement is never lost."""
+    import torch
+    out = {}
+    sections = [("rank0", _solves_rank0), ("config3_3d_slab", _solve_config3)]
+    if not args.no_batch:
+        sections.append(("config4_batch", run_batch))
+    for name, fn in sections:
+        ok = True
+        try:
+            res = fn(args, rank, world, dev)
+            if rank == 0 and res is not None:
+                if name == "rank0":
+                    out.update(res)
+                else:
+                    out[name] = res
+        except Exception as exc:
+            ok = False
+            out[name] = {"error": "%s: %s" % (type(exc).__name__, str(exc)[:300])}
+            torch.cuda.empty_cache()
+        if not _all_ok(ok, world, dev):
+            if rank == 0:
+                out.setdefault("skipped_after", name)
+            break
+    return out if rank == 0 else None
+
+
+def _solves_rank0(args, rank, world, dev):
+    """BASELINE configs[0] (2D full format) and configs[1] (3D canonical) on rank 0."""
+    import numpy as np
     import paper_1809_01971_b200 as fl
-    from paper_1809_01971_b200 import distributed as D, fullsolve, full
+    from paper_1809_01971_b200 import fullsolve
     from paper_1809_01971_b200.full import cp_dense
 
     out = {}
@@ -365,20 +452,36 @@ def run_solves(args, rank, world, dev):
         # a ~1 ms solve: median of 5 (one host hiccup otherwise dominates)
         runs = [_dev_time(lambda: fullsolve.solve_control_full(y, cfg, spec, cores=cores), 1) for _ in range(5)]
         (u, rep), t_solve = runs[0][0], float(np.median([t for _, t in runs]))
-        out["config0_2d_full"] = {"n": n, "setup_s": t_setup, "solve_s": t_solve, "solve_timing": "median of 5",
+        out["config0_2d_full"] = {"n": n, "seconds": t_setup + t_solve, "setup_s": t_setup, "solve_s": t_solve,
+                                  "solve_timing": "median of 5; seconds = setup + solve (like solve_control)",
                                   "iterations": rep.iterations,
                                   "final_residual": rep.residuals[-1], "path": "spectral PCG, 1 persistent kernel"}
-        # configs[1]: 3D canonical control solve, n=127, alpha=0.5, rank-8 bump target, eps=1e-8
+        # configs[1]: 3D canonical control solve, n=127, alpha in {0.25, 0.5, 0.75},
+        # rank-8 bump target, eps=1e-8 (operator build included, like solve_control)
         n = 127
         spec = fl.laplacian_spectrum(n, 3)
         y = fl.gaussian_bumps(n, 3, 8, seed=11)
-        cfg = fl.SolverConfig(alpha=0.5, beta=1e-2, eps=1e-8, precond_rank=6, residual_tol=1e-6, k_max=60)
-        fl.solve_control(y, cfg, spec)  # warm-up (cuSOLVER handles, kernel loads, allocator)
-        (u, rep), t = _dev_time(lambda: fl.solve_control(y, cfg, spec), 1)
-        out["config1_3d_canonical"] = {"n": n, "alpha": 0.5, "seconds": t, "iterations": rep.iterations,
-                                       "final_rank": u.rank, "final_residual": rep.residuals[-1],
+        per_alpha = {}
+        for i, alpha in enumerate((0.25, 0.5, 0.75)):
+            cfg = fl.SolverConfig(alpha=alpha, beta=1e-2, eps=1e-8, precond_rank=6, residual_tol=1e-6, k_max=60)
+            if i == 0:
+                fl.solve_control(y, cfg, spec)  # warm-up (solver handles, kernel loads, allocator)
+            (u, rep), t = _dev_time(lambda: fl.solve_control(y, cfg, spec), 1)
+            per_alpha[str(alpha)] = {"seconds": t, "iterations": rep.iterations, "final_rank": u.rank,
+                                     "final_residual": rep.residuals[-1],
+                                     "seconds_per_iteration": rep.seconds_per_iteration}
+        out["config1_3d_canonical"] = {"n": n, "per_alpha": per_alpha,
+                                       "seconds": sum(v["seconds"] for v in per_alpha.values()),
                                        "path": "canonical PCG, trunc after every step (operator build included)"}
-    # configs[3]: 3D full-format control solve, slab-partitioned over the ranks
+    return out
+
+
+def _solve_config3(args, rank, world, dev):
+    """BASELINE configs[3]: 3D full-format control solve, slab-partitioned over the ranks."""
+    import torch
+    import paper_1809_01971_b200 as fl
+    from paper_1809_01971_b200 import distributed as D, fullsolve, full
+    from paper_1809_01971_b200.full import cp_dense
     n = args.solve_n
     lay = D.SlabLayout((n, n, n), world, rank)
     spec = fl.laplacian_spectrum(n, 3)
@@ -422,13 +525,11 @@ def run_solves(args, rank, world, dev):
         (u, its, hist, conv), t_solve = _dev_time(lambda: solve(A, P), world)
         res = hist[-1]
         path = "slab-partitioned: NCCL all_to_all transposes + phase kernels with scalar all-reduces"
-    out["config3_3d_slab"] = {"n": n, "n_gpus": world, "setup_s": t_setup, "solve_s": t_solve, "iterations": its,
-                              "final_residual": res, "dof": n ** 3, "path": path}
+    rec = {"n": n, "n_gpus": world, "seconds": t_setup + t_solve, "setup_s": t_setup, "solve_s": t_solve,
+           "iterations": its, "final_residual": res, "dof": n ** 3, "path": path}
     del A, P, y, u
     torch.cuda.empty_cache()
-    if not args.no_batch:
-        out["config4_batch"] = run_batch(args, rank, world, dev)
-    return out if rank == 0 else None
+    return rec
 
 
 def run_batch(args, rank, world, dev):

@@ -50,7 +50,7 @@ int fl_sm_count(void);
 int fl_prepare(int64_t n);
 
 /* ---- spectral: orthonormal DST-I --------------------------------------
- * Replaces spectral.dst_apply (spectral.py:295-318, analytic-dst branch:
+ * Replaces spectral.dst_apply (spectral.py:163-186, analytic-dst branch:
  * scipy.fft.dst(x, type=1, norm="ortho", axis=0)) and its batched use in
  * fracop.apply (fracop.py:490-493).
  * Treats x as [outer][n][inner] and transforms the middle axis:
@@ -67,7 +67,7 @@ int fl_dst1(const double* x, double* y, int64_t outer, int64_t n, int64_t inner,
 int fl_dst1_core(const double* x, double* y, const double* core, int64_t outer, int64_t n,
                  int64_t inner, double scale, void* stream);
 
-/* Dense-eigenbasis transform (spectral.py:316-318 for generalized_mode):
+/* Dense-eigenbasis transform (spectral.py:184-186 for generalized_mode):
  * y[o] = Q^T x[o] (forward) or Q x[o] (inverse) along the middle axis, Q
  * an (n, n) row-major orthonormal matrix on the device. */
 int fl_basis_apply(const double* Q, int transpose, const double* x, double* y,
@@ -208,7 +208,8 @@ int fl_col_scale(const double* U, const double* nrm, int64_t n, int64_t R,
  * per iteration.  hist (device, k_max + 1 doubles) receives the relative
  * residual history ||r_k|| / ||b||; status (device, 4 ints) receives
  * [iterations, converged, breakdown iteration, breakdown kind (1: <R,Z> <= 0,
- * 2: <P,S> <= 0)], the reference's PcgBreakdownError conditions. */
+ * 2: <P,S> <= 0)], the reference's PcgBreakdownError conditions; on a
+ * breakdown hist[breakdown iteration] holds the offending inner product. */
 int fl_pcg_spectral(const double* b_hat, double* x_hat, double* r, double* p,
                     const double* A, const double* P, int64_t N, double tol,
                     int k_max, double* hist, int* status, void* stream);

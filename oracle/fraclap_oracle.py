@@ -20,7 +20,7 @@ TAGS = ("g1", "g2", "g3", "g4")
 # ---------------------------------------------------------------------------
 
 def laplacian_eigenvalues(n):
-    """lambda_k = (4/h^2) sin^2(pi k h / 2), k = 1..n, h = 1/(n+1) (spectral.py:232-245)."""
+    """lambda_k = (4/h^2) sin^2(pi k h / 2), k = 1..n, h = 1/(n+1) (spectral.py:100-113)."""
     n = int(n)
     h = 1.0 / (n + 1)
     k = np.arange(1, n + 1)
@@ -28,8 +28,10 @@ def laplacian_eigenvalues(n):
 
 
 def dst(x, axis=0):
-    """Orthonormal DST-I along one axis (spectral.py:312-315: scipy.fft.dst type 1, ortho)."""
-    return scipy.fft.dst(np.asarray(x, dtype=float), type=1, norm="ortho", axis=axis)
+    """Orthonormal DST-I along one axis (spectral.py:180-183: scipy.fft.dst type 1, ortho)."""
+    # workers=-1: lines are transformed independently, so the result does not
+    # depend on the thread count (bit-identical to workers=1)
+    return scipy.fft.dst(np.asarray(x, dtype=float), type=1, norm="ortho", axis=axis, workers=-1)
 
 
 def sine_matrix(n):
@@ -107,7 +109,7 @@ def required_sinc_m(a, target):
 
 # ---------------------------------------------------------------------------
 # full-format operator application (tests/oracles.py:56 dense_apply, with the
-# fast per-mode DST of spectral.py:315 instead of a dense sine matrix)
+# fast per-mode DST of spectral.py:183 instead of a dense sine matrix)
 # ---------------------------------------------------------------------------
 
 def transform_full(x):

@@ -41,6 +41,23 @@ void set_error(const char* fmt, ...);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// stream-ordered device temporary, freed on every exit path
+struct DevBuf {
+  double* p = nullptr;
+  cudaStream_t st = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  int alloc(int64_t count, cudaStream_t s) {
+    st = s;
+    FL_CUDA_TRY(cudaMallocAsync(&p, sizeof(double) * (size_t)count, s));
+    return FL_OK;
+  }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
+
 int sm_count();
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }

@@ -11,7 +11,6 @@
 #include <cudaTypedefs.h>
 
 #include "dst_fft.cuh"
-#include "dst_tma.cuh"
 #include "dst_reg.cuh"
 #include "dst_reg10.cuh"
 #include "kernels.cuh"
@@ -116,7 +115,14 @@ int get_tables(int64_t n, const Tables** out) {
   if (it == g_tables.end()) {
     Tables t;
     int rc = make_tables(n, t);
-    if (rc != FL_OK) return rc;
+    if (rc != FL_OK) {
+      // a failed build frees whatever it had allocated (no leak on retry)
+      cudaFree(t.tw);
+      cudaFree(t.sn);
+      cudaFree(t.perm);
+      cudaFree(t.sine);
+      return rc;
+    }
     it = g_tables.emplace(key, t).first;
   }
   *out = &it->second;
@@ -349,7 +355,7 @@ int launch_reg10(DstArgs a, cudaStream_t st) {
   return 1;
 }
 
-// ---- TMA-fed strided pass (dst_tma.cuh) ----------------------------------
+// ---- tensor-map encoder (driver entry point) -------------------------------
 PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static bool tried = false;
@@ -362,68 +368,6 @@ PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
       fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
   }
   return fn;
-}
-
-// returns 1 when the pass was launched, 0 when it is not TMA-eligible
-// (the caller then runs the regular kernel), < 0 on error
-template <int LOGN, bool TW3, int NBUF>
-int launch_tma(DstArgs a, const PassLayout& in, cudaStream_t st) {
-  using S = DstShape<LOGN>;
-  constexpr int NFFT = S::NFFT, NT = S::NT, C = 2 * NFFT, N = 1 << LOGN;
-  if (NT > 512) return 0;
-  auto enc = tma_encoder();
-  if (!enc) return 0;
-  a.nchunks = (a.wv + C - 1) / C;
-  a.ntiles = a.outer * a.groups * a.nchunks;
-  if (a.ntiles == 0) return 1;
-  if (a.ntiles >= (int64_t(1) << 31)) return 0;
-  a.div_blk = make_fastdiv((uint32_t)(a.groups * a.nchunks));
-  a.div_chunk = make_fastdiv((uint32_t)a.nchunks);
-  TmaGeom geo;
-  geo.box_rows = N / 2 < 256 ? N / 2 : 256;
-  geo.nbox = (N - 1 + geo.box_rows - 1) / geo.box_rows;
-  const int rowb = 16 * NFFT;
-  const int alignr = rowb >= 128 ? 1 : 128 / rowb;
-  geo.delta = alignr;
-  geo.rows_total = (geo.delta + geo.nbox * geo.box_rows + alignr - 1) / alignr * alignr;
-  geo.tx_bytes = (uint32_t)(geo.nbox * geo.box_rows * C * sizeof(double));
-  // element (o, g, c, j) at o*os + g*gp + c + j*js; dims innermost first
-  const uint64_t es = sizeof(double);
-  const uint64_t rows_b = (uint64_t)in.js * es;
-  const uint64_t grp_b = a.groups > 1 ? (uint64_t)in.gp * es : rows_b * (uint64_t)a.n;
-  const uint64_t out_b = a.outer > 1 ? (uint64_t)in.os * es : grp_b * (uint64_t)a.groups;
-  cuuint64_t dims[4] = {(cuuint64_t)a.wv, (cuuint64_t)a.n, (cuuint64_t)a.groups, (cuuint64_t)a.outer};
-  cuuint64_t strides[3] = {rows_b, grp_b, out_b};
-  cuuint32_t box[4] = {(cuuint32_t)C, (cuuint32_t)geo.box_rows, 1, 1};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUtensorMap map;
-  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(a.x), dims, strides, box, estr,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return 0;
-  const size_t smem = NBUF * (size_t)geo.rows_total * rowb + (size_t)16 * NFFT * (NT / 32) + 16 + 128;
-  if (smem > 227 * 1024) return 0;
-  auto kern = k_dst_tma<LOGN, NFFT, NT, TW3, NBUF>;
-  int grid = 0;
-  int rc = grid_for(kern, NT, smem, a.ntiles, &grid);
-  if (rc) return -rc;
-  kern<<<grid, NT, smem, st>>>(a, map, geo);
-  FL_LAUNCH_CHECK();
-  return 1;
-}
-
-template <bool TW3, int NBUF>
-int dispatch_tma(int logn, const DstArgs& a, const PassLayout& in, cudaStream_t st) {
-  switch (logn) {
-    case 6: return launch_tma<6, TW3, NBUF>(a, in, st);
-    case 7: return launch_tma<7, TW3, NBUF>(a, in, st);
-    case 8: return launch_tma<8, TW3, NBUF>(a, in, st);
-    case 9: return launch_tma<9, TW3, NBUF>(a, in, st);
-    case 10: return launch_tma<10, TW3, NBUF>(a, in, st);
-    case 11: return launch_tma<11, TW3, NBUF>(a, in, st);
-    case 12: return launch_tma<12, TW3, NBUF>(a, in, st);
-  }
-  return 0;
 }
 
 template <bool CONTIG, int LOADER, bool MID>
@@ -531,15 +475,6 @@ int dst_pass(const double* x, double* y, const double* core, int64_t n, bool con
   }
   if (core == nullptr) {
     a.scale = scale * nrm;
-    // strided tiles with 16-byte aligned rows on the input side: TMA-fed kernel
-    if (!contig && ((uintptr_t)x & 15) == 0 && in.os % 2 == 0 && in.gp % 2 == 0 && in.js % 2 == 0 &&
-        getenv("FL_TMA")) {
-      const bool db = getenv("FL_TMA")[0] == '2';
-      const int r = a.vec_out ? (db ? dispatch_tma<false, 2>(logn, a, in, st) : dispatch_tma<false, 1>(logn, a, in, st))
-                              : (db ? dispatch_tma<true, 2>(logn, a, in, st) : dispatch_tma<true, 1>(logn, a, in, st));
-      if (r < 0) return -r;
-      if (r > 0) return FL_OK;
-    }
     if (contig) return dispatch_fft<true, LOAD_PLAIN, false>(logn, a, st);
     // scalar line accesses on either side: lighter twiddle loads (measured)
     return (a.vec_in && a.vec_out) ? dispatch_fft<false, LOAD_PLAIN, false>(logn, a, st)
@@ -628,31 +563,28 @@ int dst_mode(const double* x, double* y, int64_t outer, int64_t n, int64_t inner
     if ((rc = ew_mul(y, core, y, outer * n * inner, 1.0, st))) return rc;
     return dst_pass(y, y, nullptr, n, false, outer, 1, inner, l, l, scale, st);
   }
-  // dense sine-matrix path: y_o = c * S x_o
+  // dense sine-matrix path (DMMA GEMM): y_o = c S x_o, or with a core
+  // y_o = c S (core_o .* (nrm S x_o)) with the core folded into the first
+  // GEMM's epilogue; x == y goes through a temporary
   const double nrm = std::sqrt(2.0 / (double)(n + 1));
-  const double* src = x;
-  double* tmp = nullptr;
-  if (x == y) {
-    FL_CUDA_TRY(cudaMallocAsync(&tmp, sizeof(double) * outer * n * inner, st));
-    FL_CUDA_TRY(cudaMemcpyAsync(tmp, x, sizeof(double) * outer * n * inner, cudaMemcpyDeviceToDevice, st));
-    src = tmp;
-  }
+  const int64_t total = outer * n * inner;
+  DevBuf tmp;
   if (core == nullptr) {
-    rc = gemm_f64(n, inner, n, scale * nrm, t->sine, n, 1, 0, src, inner, 1, n * inner, 0.0, y, inner, 1,
-                  n * inner, outer, st);
-  } else {
-    rc = gemm_f64(n, inner, n, nrm, t->sine, n, 1, 0, src, inner, 1, n * inner, 0.0, y, inner, 1, n * inner,
-                  outer, st);
-    if (!rc) rc = ew_mul(y, core, y, outer * n * inner, 1.0, st);
-    if (!rc) {
-      if (tmp == nullptr) FL_CUDA_TRY(cudaMallocAsync(&tmp, sizeof(double) * outer * n * inner, st));
-      FL_CUDA_TRY(cudaMemcpyAsync(tmp, y, sizeof(double) * outer * n * inner, cudaMemcpyDeviceToDevice, st));
-      rc = gemm_f64(n, inner, n, scale * nrm, t->sine, n, 1, 0, tmp, inner, 1, n * inner, 0.0, y, inner, 1,
-                    n * inner, outer, st);
+    const double* src = x;
+    if (x == y) {
+      if ((rc = tmp.alloc(total, st))) return rc;
+      FL_CUDA_TRY(cudaMemcpyAsync(tmp.p, x, sizeof(double) * total, cudaMemcpyDeviceToDevice, st));
+      src = tmp.p;
     }
+    return gemm_f64(n, inner, n, scale * nrm, t->sine, n, 1, 0, src, inner, 1, n * inner, 0.0, y, inner, 1,
+                    n * inner, outer, st);
   }
-  if (tmp) FL_CUDA_TRY(cudaFreeAsync(tmp, st));
-  return rc;
+  if ((rc = tmp.alloc(total, st))) return rc;
+  if ((rc = gemm_f64_ep(n, inner, n, nrm, t->sine, n, 1, 0, x, inner, 1, n * inner, 0.0, tmp.p, inner, 1,
+                        n * inner, outer, core, st)))
+    return rc;
+  return gemm_f64(n, inner, n, scale * nrm, t->sine, n, 1, 0, tmp.p, inner, 1, n * inner, 0.0, y, inner, 1,
+                  n * inner, outer, st);
 }
 
 // canonical apply, one mode: out[:, k*S + s] = scale * F(U[:, k] .* Xs[:, s]), out is (n, R*S)

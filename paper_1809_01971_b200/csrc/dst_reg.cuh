@@ -38,7 +38,7 @@
 #include <type_traits>
 
 #include "dst_fft.cuh"
-#include "dst_tma.cuh"
+#include "tma_util.cuh"
 
 namespace fl {
 namespace rg {

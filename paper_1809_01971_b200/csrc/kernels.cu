@@ -1,109 +1,11 @@
-// Dense fp64 building blocks: strided batched GEMM (dense sine-matrix path,
-// Gram matrices, basis transforms), core evaluation, CP expansion, sinc
-// factors and small elementwise kernels.
+// Dense fp64 building blocks: core evaluation, CP expansion, sinc factors
+// and small elementwise kernels (the DMMA GEMM is in gemm_dmma.cu).
 #include <cmath>
 
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace fl {
-
-// ---------------------------------------------------------------------------
-// strided batched GEMM, 64x64x16 tiles, 256 threads, 4x4 outputs per thread
-// ---------------------------------------------------------------------------
-struct GemmArgs {
-  int64_t M, N, K;
-  double alpha, beta;
-  const double* A;
-  int64_t sAm, sAk, bA;
-  const double* B;
-  int64_t sBk, sBn, bB;
-  double* C;
-  int64_t sCm, sCn, bC;
-};
-
-__global__ void __launch_bounds__(256) k_gemm_f64(const GemmArgs g) {
-  constexpr int BM = 64, BN = 64, BK = 16;
-  __shared__ double As[BK][BM + 1];
-  __shared__ double Bs[BK][BN + 1];
-  const int64_t b = blockIdx.z;
-  const double* A = g.A + b * g.bA;
-  const double* B = g.B + b * g.bB;
-  double* C = g.C + b * g.bC;
-  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  double acc[4][4] = {};
-  for (int64_t k0 = 0; k0 < g.K; k0 += BK) {
-    // A tile: BM x BK, B tile: BK x BN (1024 elements each, 4 per thread)
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int e = threadIdx.x + r * 256;
-      // pick the loop order that keeps consecutive threads on unit stride
-      int mm, kk;
-      if (g.sAm == 1) {
-        mm = e % BM;
-        kk = e / BM;
-      } else {
-        kk = e % BK;
-        mm = e / BK;
-      }
-      const int64_t gm = m0 + mm, gk = k0 + kk;
-      As[kk][mm] = (gm < g.M && gk < g.K) ? A[gm * g.sAm + gk * g.sAk] : 0.0;
-      int nn, kb;
-      if (g.sBn == 1) {
-        nn = e % BN;
-        kb = e / BN;
-      } else {
-        kb = e % BK;
-        nn = e / BK;
-      }
-      const int64_t gn = n0 + nn, gk2 = k0 + kb;
-      Bs[kb][nn] = (gn < g.N && gk2 < g.K) ? B[gk2 * g.sBk + gn * g.sBn] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      double av[4], bv[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) av[i] = As[kk][ty + 16 * i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx + 16 * j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t gm = m0 + ty + 16 * i;
-    if (gm >= g.M) continue;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t gn = n0 + tx + 16 * j;
-      if (gn >= g.N) continue;
-      double* c = &C[gm * g.sCm + gn * g.sCn];
-      const double v = g.alpha * acc[i][j];
-      *c = (g.beta == 0.0) ? v : fma(g.beta, *c, v);
-    }
-  }
-}
-
-int gemm_f64(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t sAm, int64_t sAk,
-             int64_t bA, const double* B, int64_t sBk, int64_t sBn, int64_t bB, double beta, double* C,
-             int64_t sCm, int64_t sCn, int64_t bC, int64_t batch, cudaStream_t st) {
-  if (M <= 0 || N <= 0 || batch <= 0) return FL_OK;
-  // plain library GEMM where cuBLAS can express the layout (about 2x the
-  // SIMT kernel below on B200: 34 vs 17 TFLOP/s at n = 1000)
-  const int rc = gemm_blas(M, N, K, alpha, A, sAm, sAk, bA, B, sBk, sBn, bB, beta, C, sCm, sCn, bC, batch, st);
-  if (rc != FL_EINVAL) return rc;
-  GemmArgs g{M, N, K, alpha, beta, A, sAm, sAk, bA, B, sBk, sBn, bB, C, sCm, sCn, bC};
-  dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64), (unsigned)batch);
-  k_gemm_f64<<<grid, 256, 0, st>>>(g);
-  FL_LAUNCH_CHECK();
-  return FL_OK;
-}
 
 // ---------------------------------------------------------------------------
 // elementwise

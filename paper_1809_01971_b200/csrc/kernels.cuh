@@ -38,10 +38,11 @@ int dst_mode(const double* x, double* y, int64_t outer, int64_t n, int64_t inner
 int dst_kr(const double* U, const double* Xs, double* out, int64_t n, int64_t R, int64_t S, double scale,
            cudaStream_t st);
 
-// C[b] = alpha * A[b] B[b] + beta * C[b] with arbitrary element strides
-int gemm_blas(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t sAm, int64_t sAk, int64_t bA,
-              const double* B, int64_t sBk, int64_t sBn, int64_t bB, double beta, double* C, int64_t sCm,
-              int64_t sCn, int64_t bC, int64_t batch, cudaStream_t st);
+// C[b] = alpha * A[b] B[b] (.* E[b]) + beta * C[b] with arbitrary element
+// strides, FP64 tensor cores (gemm_dmma.cu); E (optional) shares C's strides
+int gemm_f64_ep(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t sAm, int64_t sAk,
+                int64_t bA, const double* B, int64_t sBk, int64_t sBn, int64_t bB, double beta, double* C,
+                int64_t sCm, int64_t sCn, int64_t bC, int64_t batch, const double* E, cudaStream_t st);
 int gemm_f64(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t sAm, int64_t sAk,
              int64_t bA, const double* B, int64_t sBk, int64_t sBn, int64_t bB, double beta, double* C,
              int64_t sCm, int64_t sCn, int64_t bC, int64_t batch, cudaStream_t st);

@@ -35,7 +35,7 @@ struct PcgArgs {
   int64_t N;
   double tol;
   int kmax;
-  double* hist;        // kmax + 1 relative residuals
+  double* hist;        // kmax + 1 relative residuals (breakdown: the offending value at its iteration)
   int* status;         // [iterations, converged, breakdown iteration, breakdown kind (1: <R,Z>, 2: <P,S>)]
   double* partial;     // gridDim.x * 3 block partials
   unsigned* bar;       // [count, generation]
@@ -180,6 +180,9 @@ __global__ void __launch_bounds__(PCG_NT) k_pcg_spectral(const PcgArgs a) {
     rz = rzn;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // on breakdown the slot of the failed iteration carries the nonpositive
+    // <R,Z> or <P,S> (the value the reference reports, solver.py:154-159)
+    if (bk_kind) a.hist[bk_iter] = (bk_kind == 1) ? rz : ps;
     a.status[0] = converged ? k : (bk_kind ? bk_iter - 1 : a.kmax);
     a.status[1] = converged;
     a.status[2] = bk_iter;

@@ -46,20 +46,21 @@ __device__ __forceinline__ void rr_pair(int N, int r, int k, int& p, int& q) {
 // A: batch of m x n row-major matrices (leading dim n, batch stride m*n).
 // Outputs: U (batch, m, k), S (batch, k), Vt (batch, k, n), k = min(m, n).
 // Placement: W and V in shared memory when both fit, else V (and if need be
-// W) in a global scratch buffer (scratch != nullptr; per matrix M*K + K*K
-// doubles), which stays L2-resident for the sizes of t2c.  Vt == nullptr
+// W) in a global scratch buffer (scratch != nullptr; per matrix gstride =
+// M*K + (Vt ? K*K : 0) doubles), which stays L2-resident for the sizes of t2c.  Vt == nullptr
 // (m >= n only): left vectors and values only, no V is accumulated.
 __global__ void __launch_bounds__(SVD_THREADS) k_svd_jacobi(const double* __restrict__ A, int m, int n,
                                                             double* __restrict__ U, double* __restrict__ S,
                                                             double* __restrict__ Vt, int max_sweeps,
-                                                            double* scratch, int w_in_smem, int v_in_smem) {
+                                                            double* scratch, size_t gstride, int w_in_smem,
+                                                            int v_in_smem) {
   extern __shared__ double sm_svd[];
   const bool tr = m < n;
   const int M = tr ? n : m;  // rows of the working matrix W
   const int K = tr ? m : n;  // columns of W (= number of singular values)
   const int N = K + (K & 1);
   const bool want_v = Vt != nullptr;
-  double* gs = scratch ? scratch + (size_t)blockIdx.x * ((size_t)M * K + (size_t)K * K) : nullptr;
+  double* gs = scratch ? scratch + (size_t)blockIdx.x * gstride : nullptr;
   double* sp = sm_svd;
   double* W = w_in_smem ? sp : gs;  // column-major M x K
   if (w_in_smem) sp += (size_t)M * K;
@@ -180,7 +181,9 @@ int svd_batched(const double* A, int batch, int m, int n, double* U, double* S, 
   }
   const size_t smem = (w_sm ? wb : 0) + (v_sm ? vb : 0) + tail;
   double* scratch = nullptr;
-  if (!(w_sm && v_sm)) FL_CUDA_TRY(cudaMallocAsync(&scratch, (wb + vb) * (size_t)batch, st));
+  // per-matrix scratch stride, the same one the kernel indexes with
+  const size_t gstride = M * K + (Vt ? K * K : 0);
+  if (!(w_sm && v_sm)) FL_CUDA_TRY(cudaMallocAsync(&scratch, sizeof(double) * gstride * (size_t)batch, st));
   // function attributes are per device: one flag bit per device ordinal
   static std::atomic<uint64_t> attr_set{0};
   int dev = 0;
@@ -193,7 +196,7 @@ int svd_batched(const double* A, int batch, int m, int n, double* U, double* S, 
 #ifndef FL_SVD_SWEEPS
 #define FL_SVD_SWEEPS 40
 #endif
-  k_svd_jacobi<<<batch, SVD_THREADS, smem, st>>>(A, m, n, U, S, Vt, FL_SVD_SWEEPS, scratch, w_sm, v_sm);
+  k_svd_jacobi<<<batch, SVD_THREADS, smem, st>>>(A, m, n, U, S, Vt, FL_SVD_SWEEPS, scratch, gstride, w_sm, v_sm);
   FL_LAUNCH_CHECK();
   if (scratch) FL_CUDA_TRY(cudaFreeAsync(scratch, st));
   return FL_OK;

@@ -103,11 +103,12 @@ def pcg_full(spectrum, A, P, b, tol, k_max, mode="spectral"):
     _lib.call("fl_pcg_spectral", _lib.ptr(bh), _lib.ptr(xh), _lib.ptr(r), _lib.ptr(p), _lib.ptr(A), _lib.ptr(P),
               N, float(tol), int(k_max), _lib.ptr(hist), _lib.ptr(status), _lib.stream_ptr())
     end.record()
-    x = transform_full_from_padded(spectrum, xh) if padded else transform_full(spectrum, xh)
+    x = (transform_full_from_padded(spectrum, xh) if padded
+         else transform_full(spectrum, xh, direction="inverse"))
     st = status.cpu().numpy()
     its, conv, bk_it, bk_kind = (int(v) for v in st)
     if bk_kind:
-        raise PcgBreakdownError(bk_it, float("nan"), what="<R, Z>" if bk_kind == 1 else "<P, S>")
+        raise PcgBreakdownError(bk_it, float(hist[bk_it]), what="<R, Z>" if bk_kind == 1 else "<P, S>")
     torch.cuda.synchronize()
     secs = start.elapsed_time(end) / 1e3
     residuals = hist[: its + 1].cpu().numpy().tolist() if its else [float(hist[0])]

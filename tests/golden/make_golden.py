@@ -171,10 +171,42 @@ def config0_case():
     np.savez_compressed(os.path.join(OUT, "config0.npz"), **data)
 
 
+def config1_alpha_cases():
+    """BASELINE configs[1] at reduced n: 3D canonical control solves for every
+    alpha the config names (0.25, 0.5, 0.75), beta=1e-2, rank-8 bump target,
+    eps=1e-8, residual tol 1e-6 (reference solver.py:203-216).  n=15 and 31
+    finish in minutes on the reference; n=127 needs a 128 GiB all-pairs merge
+    matrix in the reference and is out of its reach.  One file per (n, alpha)
+    so that cases can be generated in parallel processes."""
+    sizes = [int(v) for v in os.environ.get("C1_SIZES", "15,31").split(",")]
+    alphas = [float(v) for v in os.environ.get("C1_ALPHAS", "0.25,0.5,0.75").split(",")]
+    for n3 in sizes:
+        for alpha in alphas:
+            spec3 = fraclap.laplacian_spectrum(n3, 3)
+            w, fs = _bumps(n3, 3, 8, seed=11)
+            y3 = fraclap.CpTensor(w, fs)
+            cfg3 = fraclap.SolverConfig(alpha=alpha, beta=1e-2, eps=1e-8, precond_rank=6,
+                                        residual_tol=1e-6, k_max=60)
+            t0 = time.time()
+            u3, rep3 = fraclap.solve_control(y3, cfg3, spec3)
+            dt = time.time() - t0
+            data = cp_arrays("y", y3, 3)
+            data["alpha"] = np.array(alpha)
+            data["u"] = fraclap.cp_to_dense(u3)
+            data["u_rank"] = np.array(u3.rank)
+            data["iters"] = np.array(rep3.iterations)
+            data["res"] = np.array(rep3.residuals)
+            data["seconds"] = np.array(dt)
+            name = "c1_n%d_a%02d.npz" % (n3, int(round(alpha * 100)))
+            np.savez_compressed(os.path.join(OUT, name), **data)
+            print("configs[1] n=%d alpha=%g: %d iterations, rank %d, %.1fs" % (n3, alpha, rep3.iterations,
+                                                                              u3.rank, dt), flush=True)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["spectral", "core", "apply", "trunc", "solve", "config0"]
+    which = sys.argv[1:] or ["spectral", "core", "apply", "trunc", "solve", "config0", "config1"]
     for name in which:
         t0 = time.time()
         {"spectral": spectral_cases, "core": core_cases, "apply": apply_cases, "trunc": trunc_cases,
-         "solve": solve_cases, "config0": config0_case}[name]()
+         "solve": solve_cases, "config0": config0_case, "config1": config1_alpha_cases}[name]()
         print(name, "%.1fs" % (time.time() - t0))

@@ -57,6 +57,35 @@ def test_spectral_equals_nodal_3d():
     assert rel(u1, x) <= 1e-10
 
 
+@pytest.mark.parametrize("n", [255, 511])
+def test_config3_parameters_full_solve_matches_oracle(n):
+    """BASELINE configs[3]'s parameters (alpha 0.75, beta 1e-4, 16 seeded bumps
+    + 1e-3 N(0,1) noise, rank-6 Kronecker preconditioner, tol 1e-8) at n = 255
+    and 511 (the 1023 cube needs 8.6 GB per host array): the device solve
+    (spectral persistent PCG on the padded layout, the bench path) against the
+    oracle's dense PCG (reference solver.py:116-180 without truncation) with
+    the same cores: iterations +-1, solution within 1e-8 (north_star)."""
+    spec = fl.laplacian_spectrum(n, 3)
+    cfg = fl.SolverConfig(alpha=0.75, beta=1e-4, precond_rank=6, residual_tol=1e-8, k_max=100)
+    w, f = oracle.gaussian_bumps(n, 3, 16, seed=7)
+    y = oracle.cp_to_dense(w, f) + 1e-3 * np.random.default_rng(77).standard_normal((n, n, n))
+    cores = fullsolve.control_cores(cfg, spec, layout="padded")
+    assert cores[0].shape[-1] == full.padded_pitch(n)
+    u, rep = fullsolve.solve_control_full(torch.tensor(y, device="cuda"), cfg, spec, cores=cores)
+    assert rep.converged
+    A = cores[0][..., :n].cpu().numpy()
+    P = cores[1][..., :n].cpu().numpy()
+    lam = oracle.laplacian_eigenvalues(n)
+    assert np.abs(A - oracle.dense_core("g2", [lam] * 3, 0.75, 1e-4, 1e4)).max() <= 1e-12 * np.abs(A).max()
+    del cores
+    x, hist, it, ok = oracle.pcg_dense(lambda v: oracle.apply_full(A, v), lambda v: oracle.apply_full(P, v),
+                                       y, 1e-8, 100)
+    r = rel(u, x)
+    print("configs[3] params n=%d: GPU %d its, oracle %d its, rel %.3e" % (n, rep.iterations, it, r))
+    assert ok and abs(it - rep.iterations) <= 1
+    assert r <= 1e-8
+
+
 def test_exact_preconditioner_converges_in_one_iteration():
     n = 63
     spec = fl.laplacian_spectrum(n, 3)
@@ -75,6 +104,36 @@ def test_breakdown_names_the_iteration():
     with pytest.raises(fl.PcgBreakdownError) as info:
         fullsolve.pcg_full(spec, A, P, b, 1e-8, 5)
     assert info.value.iteration == 1
+    # the reported value is the offending <P, S> = -<b, b> (reference solver.py:154-159)
+    bb = float(torch.dot(b.reshape(-1), b.reshape(-1)))
+    assert info.value.value < 0.0 and abs(info.value.value + bb) <= 1e-12 * bb
+
+
+@pytest.mark.parametrize("precond", ["identity", "exact"])
+def test_full_solve_generalized_modes(precond):
+    """Dense eigenbasis modes (Q not symmetric): the spectral solve must map
+    back with Q, not Q^T; checked against a direct dense solve."""
+    rng = np.random.default_rng(17)
+
+    def spd(n):
+        K = np.diag(2.5 + rng.uniform(0.0, 1.0, size=n))
+        off = -rng.uniform(0.1, 0.5, size=n - 1)
+        return K + np.diag(off, 1) + np.diag(off, -1)
+
+    K1, K2 = spd(7), spd(9)
+    spec = fl.EigenSpectrum((fl.generalized_mode(K1), fl.generalized_mode(K2)))
+    cfg = fl.SolverConfig(alpha=0.5, beta=0.3, gamma=1.0, residual_tol=1e-13, k_max=200)
+    y = rng.standard_normal((7, 9))
+    u, rep = fullsolve.solve_control_full(torch.tensor(y, device="cuda"), cfg, spec, precond=precond)
+    assert rep.converged
+    lam1, Q1 = np.linalg.eigh(K1)
+    lam2, Q2 = np.linalg.eigh(K2)
+    rho = lam1[:, None] + lam2[None, :]
+    g2 = cfg.beta * rho ** -0.5 + (cfg.gamma / cfg.beta) * rho ** 0.5
+    want = Q1 @ ((Q1.T @ y @ Q2) / g2) @ Q2.T
+    assert rel(u, want) <= 1e-10
+    un, _ = fullsolve.solve_control_full(torch.tensor(y, device="cuda"), cfg, spec, precond=precond, mode="nodal")
+    assert rel(un, want) <= 1e-10
 
 
 def test_zero_rhs():

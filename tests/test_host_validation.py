@@ -1,5 +1,5 @@
 """CPU suite: host-side argument validation mirrors the reference's ValueErrors
-(tests/test_fracop.py:29-44, test_decomp.py:40-50, test_solver.py:422-431)."""
+(tests/test_fracop.py:29-44, test_decomp.py:40-50, test_solver.py:40-62)."""
 
 import numpy as np
 import pytest

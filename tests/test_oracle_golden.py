@@ -33,7 +33,7 @@ def test_eigenvalues_and_dst_match_reference():
 
 
 def test_frozen_small_values():
-    # reference tests/test_spectral.py:148-154 and SPEC examples
+    # reference tests/test_spectral.py:16-24 and SPEC examples
     assert np.allclose(oracle.laplacian_eigenvalues(2), [9.0, 27.0], atol=1e-12)
     assert np.allclose(oracle.laplacian_eigenvalues(3), [9.372583002030, 32.0, 54.627416997970], atol=1e-9)
     lam = oracle.laplacian_eigenvalues(2)
@@ -94,7 +94,7 @@ def test_cp_inner_and_normalize():
         assert oracle.cp_inner(wa, fa, wb, fb) == pytest.approx(float(np.vdot(da, db)), rel=1e-12)
         w2, f2 = oracle.cp_normalize(wa, fa)
         assert rel(oracle.cp_to_dense(w2, f2), da) <= 1e-13
-    # 3-4-5 and zero-column cases (reference tests/test_tensor.py:313-331)
+    # 3-4-5 and zero-column cases (reference tests/test_tensor.py:71-90)
     w, f = oracle.cp_normalize(np.array([2.0]), [np.array([[3.0], [4.0]]), np.array([[4.0], [3.0]])])
     assert w[0] == pytest.approx(50.0)
     w, f = oracle.cp_normalize(np.array([1.0, 3.0]), [np.array([[0.0, 1.0], [0.0, 2.0]]),
