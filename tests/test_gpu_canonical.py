@@ -147,7 +147,7 @@ def test_solve_control_3d_golden(n3):
     u, rep = fl.solve_control(y, cfg, spec)
     assert rep.converged
     assert abs(rep.iterations - int(g[key + "_iters"])) <= 1
-    assert rel(fl.cp_to_dense(u), g[key + "_u"]) <= 1e-6
+    assert rel(fl.cp_to_dense(u), g[key + "_u"]) <= 1e-8  # measured 1e-14 .. 5e-12 (r2)
 
 
 C1_CASES = sorted(f[:-4] for f in os.listdir(os.path.join(os.path.dirname(__file__), "golden"))
@@ -161,7 +161,8 @@ def test_config1_alpha_golden(case):
     (reference solver.py:203-216; beta 1e-2, eps 1e-8, tol 1e-6) vs the
     reference's own solution.  Iterations +-1; the solution difference is
     bounded by the truncation both sides apply after every PCG step (eps =
-    1e-8 per trunc, several truncs per iteration) and is reported."""
+    1e-8 per trunc, several truncs per iteration) and is reported.  Measured
+    on B200 (r2): 3e-14 .. 5e-12, so the north_star 1e-8 bound is asserted."""
     g = load(case)
     n = g["y_f0"].shape[0]
     spec = fl.laplacian_spectrum(n, 3)
@@ -180,7 +181,7 @@ def test_config1_alpha_golden(case):
                                                rel(got, u_exact), rel(want, u_exact)))
     assert rep.converged
     assert abs(rep.iterations - int(g["iters"])) <= 1
-    assert r <= 1e-6
+    assert r <= 1e-8
 
 
 def test_merge_collinear_matches_all_pairs_rule():

@@ -16,6 +16,8 @@ for nm in ("apply", "apply_compressed", "build_core", "reciprocal_core"):
     if hasattr(fracop, nm): wrap(fracop, nm, "fracop." + nm)
 for nm in ("apply", "apply_compressed", "build_preconditioner", "trunc", "cp_inner"):
     if hasattr(solver, nm): wrap(solver, nm, "solver." + nm)
+for nm in ("control_core_expsum", "preconditioner_coarse", "pcg", "trunc", "multigrid_tucker", "t2c"):
+    wrap(batch, nm, "batch." + nm)
 n = int(sys.argv[1])
 list(batch.solve_batch(n, 1))  # warm-up
 stats.clear()
