@@ -569,6 +569,23 @@ int dst_mode(const double* x, double* y, int64_t outer, int64_t n, int64_t inner
   const double nrm = std::sqrt(2.0 / (double)(n + 1));
   const int64_t total = outer * n * inner;
   DevBuf tmp;
+  if (inner == 1) {
+    // lines: Y (outer x n) = X S (S symmetric, read N-major)
+    const double* src = x;
+    if (x == y || core != nullptr) {
+      if ((rc = tmp.alloc(total, st))) return rc;
+    }
+    if (core != nullptr) {
+      if ((rc = gemm_f64_ep(outer, n, n, nrm, x, n, 1, 0, t->sine, n, 1, 0, 0.0, tmp.p, n, 1, 0, 1, core, st)))
+        return rc;
+      return gemm_f64(outer, n, n, scale * nrm, tmp.p, n, 1, 0, t->sine, n, 1, 0, 0.0, y, n, 1, 0, 1, st);
+    }
+    if (x == y) {
+      FL_CUDA_TRY(cudaMemcpyAsync(tmp.p, x, sizeof(double) * total, cudaMemcpyDeviceToDevice, st));
+      src = tmp.p;
+    }
+    return gemm_f64(outer, n, n, scale * nrm, src, n, 1, 0, t->sine, n, 1, 0, 0.0, y, n, 1, 0, 1, st);
+  }
   if (core == nullptr) {
     const double* src = x;
     if (x == y) {

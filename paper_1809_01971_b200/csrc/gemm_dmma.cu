@@ -40,6 +40,8 @@ struct DmmaArgs {
   double* C;
   int64_t sCm, sCn, bC;
   const double* E;  // optional epilogue factor with C's strides
+  int64_t nfast;    // tiles of the faster-varying grid dimension
+  int n_fast;       // 1: N tiles vary fastest along blockIdx.x, 0: M tiles
 };
 
 __device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, double b) {
@@ -55,7 +57,11 @@ __global__ void __launch_bounds__(GNT) k_gemm_dmma(const DmmaArgs g) {
   const int64_t b = blockIdx.z;
   const double* __restrict__ A = g.A + b * g.bA;
   const double* __restrict__ B = g.B + b * g.bB;
-  const int64_t m0 = (int64_t)blockIdx.x * GBM, n0 = (int64_t)blockIdx.y * GBN;
+  // linear tile index, the operand dimension with fewer tiles fastest: the
+  // CTAs that run together share the slab of the larger operand (one DRAM
+  // read, then L2 hits)
+  const int64_t tl = blockIdx.x, tf = tl % g.nfast, ts = tl / g.nfast;
+  const int64_t m0 = (g.n_fast ? ts : tf) * GBM, n0 = (g.n_fast ? tf : ts) * GBN;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
 
@@ -163,10 +169,12 @@ int gemm_f64_ep(int64_t M, int64_t N, int64_t K, double alpha, const double* A, 
     // C'[b, m] = sum_k B[b][k] A[m, k]  (M' = batch, N' = M)
     return gemm_f64_ep(batch, M, K, alpha, B, bB, sBk, 0, A, sAk, sAm, 0, beta, C, bC, sCm, 0, 1, E, st);
   }
-  FL_ARG_CHECK(batch <= 65535 && (N + GBN - 1) / GBN <= 65535 && (M + GBM - 1) / GBM < (int64_t)1 << 31,
-               "GEMM grid too large (M %lld, N %lld, batch %lld)", (long long)M, (long long)N, (long long)batch);
-  DmmaArgs g{M, N, K, alpha, beta, A, sAm, sAk, bA, B, sBk, sBn, bB, C, sCm, sCn, bC, E};
-  const dim3 grid((unsigned)((M + GBM - 1) / GBM), (unsigned)((N + GBN - 1) / GBN), (unsigned)batch);
+  const int64_t mt = (M + GBM - 1) / GBM, nt = (N + GBN - 1) / GBN;
+  FL_ARG_CHECK(batch <= 65535 && mt * nt < ((int64_t)1 << 31), "GEMM grid too large (M %lld, N %lld, batch %lld)",
+               (long long)M, (long long)N, (long long)batch);
+  const int n_fast = nt <= mt ? 1 : 0;
+  DmmaArgs g{M, N, K, alpha, beta, A, sAm, sAk, bA, B, sBk, sBn, bB, C, sCm, sCn, bC, E, n_fast ? nt : mt, n_fast};
+  const dim3 grid((unsigned)(mt * nt), 1u, (unsigned)batch);
   const bool ak = (sAk == 1), bn = (sBn == 1);
   if (ak && bn)
     k_gemm_dmma<true, true><<<grid, GNT, 0, st>>>(g);

@@ -4,6 +4,7 @@ import sys
 import time
 import collections
 import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1809_01971_b200 as fl
 from paper_1809_01971_b200 import decomp, fracop, solver
 
