@@ -170,7 +170,7 @@ def _solve_one(i, n, spec, max_level):
             "residual": rep.residuals[-1]}
 
 
-def solve_batch(n, count, rank=0, world=1, max_level=1023, concurrency=1):
+def solve_batch(n, count, rank=0, world=1, max_level=1023, concurrency=1, serial_linalg=True):
     """Solve problems rank, rank+world, ... of the batch; returns per-problem
     records (in problem order).
 
@@ -194,5 +194,11 @@ def solve_batch(n, count, rank=0, world=1, max_level=1023, concurrency=1):
         with torch.cuda.stream(_tls.stream):
             return _solve_one(i, n, spec, max_level)
 
-    with ThreadPoolExecutor(max_workers=int(concurrency)) as pool:
-        return list(pool.map(task, idx))
+    from .decomp import _LaSerial
+    prev = _LaSerial.enabled
+    _LaSerial.enabled = serial_linalg
+    try:
+        with ThreadPoolExecutor(max_workers=int(concurrency)) as pool:
+            return list(pool.map(task, idx))
+    finally:
+        _LaSerial.enabled = prev

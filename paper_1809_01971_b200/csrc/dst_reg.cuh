@@ -182,7 +182,6 @@ __device__ __forceinline__ Tile tile_of(const DstArgs& a, uint32_t t) {
   return r;
 }
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 // cp.async with a compile-time shared-memory offset; sz = 0 zero-fills
 template <int OFF>
@@ -260,31 +259,36 @@ __device__ __forceinline__ void issue_strided(const DstArgs& a, uint32_t t, uint
 // would be past the line, possibly past the tensor).
 __device__ __forceinline__ int line_shift(const Tile& tl, int l) { return (int)((tl.base + l * tl.LS) & 1); }
 
-__device__ __forceinline__ void issue_contig(const DstArgs& a, uint32_t t, uint32_t stile, int w, int lane) {
+__device__ __forceinline__ void issue_contig_tile(const double* x, const Tile& tl, uint32_t stile, int w, int lane) {
   if (FL_REG_NOMEM == 1 || FL_REG_NOMEM == 2) return;
-  const Tile tl = tile_of<SIDE_CONTIG, false>(a, t);
   const uint32_t d = stile + 8u * (uint32_t)(4 * w * 512) + 16u * (uint32_t)lane;
   static_for<0, 4>([&](auto L) {
     constexpr int l = decltype(L)::value;
     const bool ok = 4 * w + l < tl.lmax;
     const int sh = line_shift(tl, 4 * w + l);
-    const double* src = ok ? a.x + tl.base + (int64_t)(4 * w + l) * tl.LS - sh + 2 * lane : a.x;
+    const double* src = ok ? x + tl.base + (int64_t)(4 * w + l) * tl.LS - sh + 2 * lane : x;
     const int sz = ok ? 16 : 0;
     const int szl = ok ? (sh ? 16 : (lane == 31 ? 8 : 16)) : 0;
     static_for<0, 8>([&](auto I) {
       constexpr int i = decltype(I)::value;
-      cp16<8 * (l * 512 + 64 * i)>(d, ok ? src + 64 * i : a.x, i == 7 ? szl : sz);
+      cp16<8 * (l * 512 + 64 * i)>(d, ok ? src + 64 * i : x, i == 7 ? szl : sz);
     });
   });
+}
+
+__device__ __forceinline__ void issue_contig(const DstArgs& a, uint32_t t, uint32_t stile, int w, int lane) {
+  issue_contig_tile(a.x, tile_of<SIDE_CONTIG, false>(a, t), stile, w, lane);
 }
 
 // A warp's 4 lines as one bulk copy when they are one contiguous,
 // 16-byte aligned blob: pitch 512 (padded, 16 KB) or the dense pitch 511
 // (16352 B; the blob starts at line 16t + 4w, an even line, so at a 16-byte
 // aligned offset).  The ragged last tile keeps cp.async (zero fill).
-__device__ __forceinline__ bool contig_bulk(const DstArgs& a, const Tile& tl, int w) {
-  return (tl.LS == 511 || tl.LS == 512) && 4 * w + 3 < tl.lmax && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
+__device__ __forceinline__ bool contig_bulk_p(const double* x, const Tile& tl, int w) {
+  return (tl.LS == 511 || tl.LS == 512) && 4 * w + 3 < tl.lmax && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) &&
+         ((tl.base + (int64_t)(4 * w) * tl.LS) & 1) == 0;
 }
+__device__ __forceinline__ bool contig_bulk(const DstArgs& a, const Tile& tl, int w) { return contig_bulk_p(a.x, tl, w); }
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -294,18 +298,21 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 }
 
 // contiguous tile issue: bulk copy (lane 0, completes on wbar) or cp.async
-__device__ __forceinline__ void issue_contig_any(const DstArgs& a, uint32_t t, double2* tile, uint32_t stile, int w,
-                                                 int lane, uint64_t* wbar) {
-  const Tile tl = tile_of<SIDE_CONTIG, false>(a, t);
-  if (contig_bulk(a, tl, w)) {
+__device__ __forceinline__ void issue_contig_any_tile(const double* x, const Tile& tl, double2* tile, uint32_t stile,
+                                                      int w, int lane, uint64_t* wbar) {
+  if (contig_bulk_p(x, tl, w)) {
     if (lane == 0 && !(FL_REG_NOMEM == 1 || FL_REG_NOMEM == 2)) {
       const uint32_t bytes = (uint32_t)(4 * tl.LS * sizeof(double));
       mbar_expect_tx(wbar, bytes);
-      bulk_load(tile + 1024 * w, a.x + tl.base + (int64_t)(4 * w) * tl.LS, bytes, wbar);
+      bulk_load(tile + 1024 * w, x + tl.base + (int64_t)(4 * w) * tl.LS, bytes, wbar);
     }
   } else {
-    issue_contig(a, t, stile, w, lane);
+    issue_contig_tile(x, tl, stile, w, lane);
   }
+}
+__device__ __forceinline__ void issue_contig_any(const DstArgs& a, uint32_t t, double2* tile, uint32_t stile, int w,
+                                                 int lane, uint64_t* wbar) {
+  issue_contig_any_tile(a.x, tile_of<SIDE_CONTIG, false>(a, t), tile, stile, w, lane, wbar);
 }
 
 struct Lane {
@@ -609,9 +616,9 @@ __device__ __forceinline__ void store_strided(const DstArgs& a, uint32_t t, doub
 // stored as 16 bytes where the line is 16-byte aligned.
 __device__ __forceinline__ int cstg(int p) { return (((p >> 1) ^ ((p >> 5) & 7)) << 1) | (p & 1); }
 
-__device__ __forceinline__ void store_contig(const DstArgs& a, uint32_t t, double2* scr, int w, int lane, int f,
-                                             int q, const double2 (&ev)[16], const double2 (&od)[16], double sc) {
-  const Tile tl = tile_of<SIDE_CONTIG, true>(a, t);
+__device__ __forceinline__ void store_contig_tile(const DstArgs& a, double* yout, const Tile& tl, double2* scr, int w,
+                                                  int lane, int f, int q, const double2 (&ev)[16],
+                                                  const double2 (&od)[16], double sc) {
   double* sd = reinterpret_cast<double*>(scr);
   double* la = sd + (2 * f) * 256;  // line 2f (.x), line 2f + 1 (.y) at + 256
 #pragma unroll 1
@@ -642,8 +649,8 @@ __device__ __forceinline__ void store_contig(const DstArgs& a, uint32_t t, doubl
       for (int l = 0; l < 4; ++l) {
         if (4 * w + l < tl.lmax) {
           const int64_t off = tl.base + (int64_t)(4 * w + l) * tl.LS + 256 * hh;  // element of position 256 hh
-          const bool al = ((off & 1) == 0) && ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0);
-          double* y = a.y + off;
+          const bool al = ((off & 1) == 0) && ((reinterpret_cast<uintptr_t>(yout) & 15) == 0);
+          double* y = yout + off;
 #pragma unroll
           for (int s = 0; s < 4; ++s) {
             const int c = lane + 32 * s;  // chunk: positions 2c, 2c + 1 of the half
@@ -662,6 +669,11 @@ __device__ __forceinline__ void store_contig(const DstArgs& a, uint32_t t, doubl
     }
     __syncwarp();
   }
+}
+
+__device__ __forceinline__ void store_contig(const DstArgs& a, uint32_t t, double2* scr, int w, int lane, int f,
+                                             int q, const double2 (&ev)[16], const double2 (&od)[16], double sc) {
+  store_contig_tile(a, a.y, tile_of<SIDE_CONTIG, true>(a, t), scr, w, lane, f, q, ev, od, sc);
 }
 
 // ---- TMA tensor stores of strided outputs ---------------------------------
@@ -703,14 +715,10 @@ __device__ __forceinline__ int stg_tma_idx(int hh, int qq, int ii, int ch) {
 // DEFER: half 1's staging is drained by the kernel before the next exchange
 // instead of here (measured: helps the fused pass, costs the plain one)
 template <bool DEFER>
-__device__ __forceinline__ void store_strided_tma(const DstArgs& a, const OutMaps* maps, uint32_t t, double2* stg,
-                                                  int w, int f, int q, const double2 (&ev)[16],
-                                                  const double2 (&od)[16]) {
+__device__ __forceinline__ void store_strided_tma_at(const OutMaps* maps, int c0, uint32_t g, uint32_t o, double2* stg,
+                                                     int w, int f, int q, const double2 (&ev)[16],
+                                                     const double2 (&od)[16]) {
   const int ch = 2 * w + f;
-  const uint32_t o = a.div_blk.div(t);
-  const uint32_t rr = t - o * a.div_blk.d;
-  const uint32_t g = a.div_chunk.div(rr);
-  const int c0 = (int)(rr - g * a.div_chunk.d) * 16;
   // the staging interleaves all four warps' columns over the whole 32 KB of
   // scratch: every warp must be done with its exchange/spectrum first
   __syncthreads();
@@ -740,18 +748,33 @@ __device__ __forceinline__ void store_strided_tma(const DstArgs& a, const OutMap
   }
 }
 
+template <bool DEFER>
+__device__ __forceinline__ void store_strided_tma(const DstArgs& a, const OutMaps* maps, uint32_t t, double2* stg,
+                                                  int w, int f, int q, const double2 (&ev)[16],
+                                                  const double2 (&od)[16]) {
+  const uint32_t o = a.div_blk.div(t);
+  const uint32_t rr = t - o * a.div_blk.d;
+  const uint32_t g = a.div_chunk.div(rr);
+  const int c0 = (int)(rr - g * a.div_chunk.d) * 16;
+  store_strided_tma_at<DEFER>(maps, c0, g, o, stg, w, f, q, ev, od);
+}
+
 // TMA load of strided tile t: two 256-row boxes of 16 columns, rows -1 ..
 // 254 (row -1 out of range: zeros) and 255 .. 510 into tile rows 0 .. 511;
 // the 128-byte swizzle is exactly tidx's chunk ^ (row & 7)
+__device__ __forceinline__ void tma_issue_at(const CUtensorMap* map, int c0, int g, int o, double2* tile,
+                                             uint64_t* bar) {
+  mbar_expect_tx(bar, (uint32_t)(TILE * sizeof(double2)));
+  tma_load_4d(tile, map, c0, -1, g, o, bar);
+  tma_load_4d(tile + TILE / 2, map, c0, 255, g, o, bar);
+}
 __device__ __forceinline__ void tma_issue_grp(const DstArgs& a, const CUtensorMap* map, uint32_t t, double2* tile,
                                               uint64_t* bar) {
   const uint32_t o = a.div_blk.div(t);
   const uint32_t r = t - o * a.div_blk.d;
   const uint32_t g = a.div_chunk.div(r);
   const int c0 = (int)(r - g * a.div_chunk.d) * 16;
-  mbar_expect_tx(bar, (uint32_t)(TILE * sizeof(double2)));
-  tma_load_4d(tile, map, c0, -1, (int)g, (int)o, bar);
-  tma_load_4d(tile + TILE / 2, map, c0, 255, (int)g, (int)o, bar);
+  tma_issue_at(map, c0, (int)g, (int)o, tile, bar);
 }
 
 // Persistent CTAs of 4 warps (one 16-line tile at a time), 2 per SM.

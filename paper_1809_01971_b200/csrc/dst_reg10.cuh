@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(32 * NW, 8 / NW) k_dst_reg10(const DstArgs a, 
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint64_t* const wbar = bar + 1 + w;
   double2* const scr = scr_all + SCR * w;
-  const uint32_t stile = rg::smem_u32(tile);
+  const uint32_t stile = smem_u32(tile);
   const uint32_t ntiles = (uint32_t)a.ntiles * PIECES;
   constexpr bool STRIDED = SIDE_IN != SIDE_CONTIG;
   if (STRIDED && (stile & 1023u) != 0) __trap();
