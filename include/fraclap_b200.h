@@ -125,20 +125,9 @@ int fl_apply_full_padded(const double* x, double* y, const double* core_p, doubl
  * covers columns i2 = 16c + 4w .. 16c + 4w + 3; entry ((u * 32 + i) * 32
  * + 16 f + q) is the double pair (G[r - 1][i1][16c + 4w + 2f],
  * G[r - 1][i1][16c + 4w + 2f + 1]), r = 32q + i (r = 0 gives zeros).
- * work: [511][n1][512] doubles, padding zero-initialised once.
- * For the 511^3 cube (n1 = 511) the two plain passes on each side are
- * fused per i0-plane (fl_dst1_plane_pair): 3 launches, 56 B/DoF. */
+ * work: [511][n1][512] doubles, padding zero-initialised once. */
 int fl_apply_full_lanes(const double* x, double* y, const double* core_l, double* work,
                         int d, const int64_t* dims, double alpha, void* stream);
-
-/* Plane-fused pass pair of the 511^3 lane apply (per-pass timing):
- * inverse == 0: last mode of the dense x (pitch 511) then mode 1, per
- * i0-plane, into the padded work tensor y ([511][511][512]); the plane
- * between the two transforms lives in a 16-slot ring that stays in L2.
- * inverse != 0: mode 1 then last mode, padded x -> dense y, scaled by
- * alpha.  x != y.  Replaces the reference's per-mode dst_apply loop
- * (spectral.py:163-186) for two of the three modes of a 511^3 tensor. */
-int fl_dst1_plane_pair(const double* x, double* y, int inverse, double alpha, void* stream);
 
 /* The fused mode-0 pass of fl_apply_full_lanes on its own (per-pass timing):
  * y = scale * F_0 diag(core_l) F_0 x on [511][groups][512], x == y allowed. */

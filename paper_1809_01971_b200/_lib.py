@@ -46,7 +46,6 @@ SIGNATURES = {
     "fl_apply_full_lanes": (c_int, [c_vp, c_vp, c_vp, c_vp, c_int, P(c_i64), c_dbl, c_vp]),
     "fl_dst1_core_lanes": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_dbl, c_vp]),
     "fl_dst1_core_lanes_mode0": (c_int, [c_vp, c_vp, c_vp, c_i64, c_dbl, c_vp]),
-    "fl_dst1_plane_pair": (c_int, [c_vp, c_vp, c_int, c_dbl, c_vp]),
     "fl_dst1_pass": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_i64, c_i64, c_i64, P(c_i64), P(c_i64), c_dbl, c_vp]),
     "fl_transform_full": (c_int, [c_vp, c_vp, c_int, P(c_i64), c_dbl, c_vp]),
     "fl_cp_apply_mode": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_dbl, c_vp]),

@@ -157,13 +157,6 @@ int fl_apply_full_lanes(const double* x, double* y, const double* core_l, double
   const int64_t lines = n0 * n1;  // lines of the last mode
   cudaStream_t st = as_stream(stream);
   // last mode first, contiguous: dense rows (pitch 511) -> padded rows (512)
-  if (d == 3 && n1 == 511 && plane_enabled()) {
-    // 3 launches, 56 B/DoF: last mode + mode 1 through the L2 ring, mode 0
-    // fused with the core, mode 1 + last mode back through the ring
-    if ((rc = dst_plane_pair(true, x, work, 1.0, st))) return rc;
-    if ((rc = dst_pass_lanes_mode0(work, work, core_l, n1, 1.0, st))) return rc;
-    return dst_plane_pair(false, work, y, alpha, st);
-  }
   const PassLayout dense_l{0, 1, 0, nl}, pad_l{0, 1, 0, P};
   // (writes the padding position too: pass 2 and the fused pass pair the last
   // column with it in one packed FFT)
@@ -174,10 +167,6 @@ int fl_apply_full_lanes(const double* x, double* y, const double* core_l, double
   if ((rc = dst_pass_lanes_mode0(work, work, core_l, n1, 1.0, st))) return rc;
   if (d == 3 && (rc = dst_pass(work, work, nullptr, n1, false, n0, 1, P, mid, mid, 1.0, st))) return rc;
   return dst_pass(work, y, nullptr, nl, true, lines, 1, 1, pad_l, dense_l, alpha, st);
-}
-
-int fl_dst1_plane_pair(const double* x, double* y, int inverse, double alpha, void* stream) {
-  return dst_plane_pair(inverse == 0, x, y, alpha, as_stream(stream));
 }
 
 int fl_dst1_core_lanes_mode0(const double* x, double* y, const double* core_l, int64_t groups, double scale,

@@ -13,7 +13,6 @@
 #include "dst_fft.cuh"
 #include "dst_reg.cuh"
 #include "dst_reg10.cuh"
-#include "dst_plane.cuh"
 #include "kernels.cuh"
 
 namespace fl {
@@ -541,79 +540,6 @@ int dst_pass_lanes(const double* x, double* y, const double* core_l, int64_t lin
   a.sn = t->sn;
   a.scale = scale * nrm * nrm;
   return launch_reg<rg::SIDE_CONTIG, rg::SIDE_CONTIG, true>(a, st);
-}
-
-// Plane-fused pair of passes on a 511^3 tensor (dst_plane.cuh): forward =
-// last mode (dense x, pitch 511) then mode 1, into the padded work tensor;
-// inverse = mode 1 then last mode, padded work -> dense y scaled by alpha.
-int dst_plane_pair(bool fwd, const double* x, double* y, double alpha, cudaStream_t st) {
-  FL_ARG_CHECK(x != nullptr && y != nullptr && x != y, "plane pass: distinct input and output required");
-  auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
-  FL_ARG_CHECK(al(x) && al(y), "plane pass: 16-byte aligned buffers required");
-  const Tables* t = nullptr;
-  int rc = get_tables(511, &t);
-  if (rc) return rc;
-  const double nrm = std::sqrt(2.0 / 512.0);
-  DevBuf ring, sync;
-  if ((rc = ring.alloc((int64_t)pl::RING_LINES * pl::PITCH, st))) return rc;
-  if ((rc = sync.alloc(pl::NP + 8, st))) return rc;  // ready[511], consumed[511], ticket (ints)
-  int* ctr = reinterpret_cast<int*>(sync.p);
-  FL_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(int) * (2 * pl::NP + 2), st));
-  pl::PlaneArgs P{};
-  P.a.n = 511;
-  P.a.tw = t->tw;
-  P.a.sn = t->sn;
-  P.a.scale = 1.0;
-  P.a.pad_zero = fwd ? 1 : 0;
-  P.x = x;
-  P.y = y;
-  P.ring = ring.p;
-  P.ready = ctr;
-  P.consumed = ctr + pl::NP;
-  P.ticket = reinterpret_cast<unsigned*>(ctr + 2 * pl::NP);
-  P.scale_a = nrm;
-  P.scale_b = fwd ? nrm : alpha * nrm;
-  // tensor maps: the plane-chunk side reads the ring (forward) or the work
-  // tensor (inverse), rows of 512 doubles, planes of 511 rows; it writes the
-  // work tensor (forward) or the ring (inverse)
-  const int64_t plane = (int64_t)pl::NP * pl::PITCH;
-  DstArgs m{};
-  m.n = 511;
-  m.wv = pl::PITCH;
-  m.groups = 1;
-  m.in_js = m.out_js = pl::PITCH;
-  m.in_os = m.out_os = plane;
-  m.x = fwd ? ring.p : x;
-  m.outer = fwd ? pl::SLOTS : pl::NP;
-  CUtensorMap mapL{};
-  FL_ARG_CHECK(reg_tensor_map(m, &mapL), "plane pass: tensor map encoding failed");
-  m.y = fwd ? y : ring.p;
-  m.outer = fwd ? pl::NP : pl::SLOTS;
-  rg::OutMaps om{};
-  FL_ARG_CHECK(reg_out_maps(m, &om), "plane pass: output tensor maps failed");
-  constexpr size_t SMEM = pl::plane_smem_bytes();
-  auto kern = fwd ? pl::k_plane<true> : pl::k_plane<false>;
-  static std::atomic<uint64_t> attr_set{0};
-  int dev = 0;
-  FL_CUDA_TRY(cudaGetDevice(&dev));
-  const uint64_t bit = uint64_t(1) << (dev & 63);
-  if (!(attr_set.load() & bit)) {
-    FL_CUDA_TRY(cudaFuncSetAttribute(pl::k_plane<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
-    FL_CUDA_TRY(cudaFuncSetAttribute(pl::k_plane<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
-    attr_set.fetch_or(bit);
-  }
-  kern<<<2 * sm_count(), 32 * rg::NWARP, SMEM, st>>>(P, mapL, om);
-  FL_LAUNCH_CHECK();
-  return FL_OK;
-}
-
-bool plane_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("FL_PLANE");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1 && reg_enabled();
 }
 
 // y = scale * F_n x along the middle axis (optionally core-scaled sandwich)

@@ -29,12 +29,6 @@ int dst_pass_lanes(const double* x, double* y, const double* core_l, int64_t lin
 int dst_pass_lanes_mode0(const double* x, double* y, const double* core_l, int64_t groups, double scale,
                          cudaStream_t st);
 
-// plane-fused pass pair on a 511^3 tensor (dst_plane.cuh): fwd = last mode
-// (dense pitch 511) + mode 1 into the padded layout; inverse = mode 1 + last
-// mode back to dense, scaled by alpha
-int dst_plane_pair(bool fwd, const double* x, double* y, double alpha, cudaStream_t st);
-bool plane_enabled();
-
 // y = scale * F x along the middle axis of [outer][n][inner]; with core != nullptr
 // y = scale * F diag(core) F x (core in the layout of x)
 int dst_mode(const double* x, double* y, int64_t outer, int64_t n, int64_t inner, double scale,

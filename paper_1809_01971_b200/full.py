@@ -310,11 +310,10 @@ class FullOperator:
                   len(self.dims), _lib.dims_arr(self.dims), self.pitch, self.alpha, _lib.stream_ptr())
         return y
 
-    def passes(self, x, y, plane=None):
+    def passes(self, x, y):
         """The DST passes of one application as (name, fl_dst1_pass args)
         tuples, in launch order (for per-pass timing; same launches as
-        __call__ on a padded operator).  plane=False lists the five separate
-        passes of the 511^3 lane apply instead of its plane-fused pairs."""
+        __call__ on a padded operator)."""
         if not self.padded:
             raise ValueError("per-pass list is defined for the padded layout")
         dims, P = tuple(self.dims), self.pitch
@@ -325,13 +324,6 @@ class FullOperator:
             # fl_apply_full_lanes: last mode contiguous (dense rows -> padded),
             # mode 1, mode 0 fused with the core, mode 1, last mode back
             n1 = dims[1] if len(dims) == 3 else 1
-            if plane is None:
-                plane = os.environ.get("FL_PLANE", "1") != "0"
-            if n1 == 511 and plane:
-                # the 511^3 cube: plane-fused pass pairs around the mode-0 pass
-                return [("dst_plane_fwd", ("plane", xp, wp, 0, 1.0)),
-                        ("dst_core_mode0", ("lanes0", wp, wp, cp, n1, 1.0)),
-                        ("dst_plane_inv", ("plane", wp, yp, 1, self.alpha))]
             lines = dims[0] * n1
             dl, pl = (0, 1, 0, nl), (0, 1, 0, P)
             mid = (n1 * P, P, 0, 0)
@@ -370,10 +362,6 @@ def run_pass(args, stream=None):
     if args[0] == "lanes":
         _, x, y, c, lines, pitch, scale = args
         _lib.call("fl_dst1_core_lanes", x, y, c, lines, pitch, float(scale), s)
-        return
-    if args[0] == "plane":
-        _, x, y, inv, alpha = args
-        _lib.call("fl_dst1_plane_pair", x, y, int(inv), float(alpha), s)
         return
     if args[0] == "lanes0":
         _, x, y, c, groups, scale = args

@@ -172,39 +172,6 @@ def test_apply_511_cube_matches_oracle(kind):
     assert rel_l2 <= 1e-10 and max_rel <= 1e-10
 
 
-def test_plane_fused_apply_equals_separate_passes():
-    """The 511^3 apply through the plane-fused pass pairs (L2 ring, dynamic
-    ticket schedule) is bit-identical to the five separate passes: every tile
-    runs the same arithmetic, only the intermediate's home and the schedule
-    differ.  Repeated applies are bit-identical too (schedule-independent)."""
-    n = 511
-    spec = spectral.laplacian_spectrum(n, 3)
-    op = full.FullOperator.from_kind(CoreFunctionKind("g2", 0.5, coeff_minus=0.3, coeff_plus=2.0), spec)
-    g = torch.Generator(device="cuda")
-    g.manual_seed(11)
-    x = torch.randn((n, n, n), dtype=torch.float64, device="cuda", generator=g)
-    fused = op.passes(x, torch.empty_like(x), plane=True)
-    assert [nm for nm, _ in fused] == ["dst_plane_fwd", "dst_core_mode0", "dst_plane_inv"]
-    y1 = op(x)
-    y2 = torch.empty_like(x)
-    for _, a in op.passes(x, y2, plane=False):
-        full.run_pass(a)
-    y3 = torch.empty_like(x)
-    for _, a in op.passes(x, y3, plane=True):
-        full.run_pass(a)
-    assert torch.equal(y1, y2) and torch.equal(y1, y3)
-    for _ in range(3):
-        assert torch.equal(op(x), y1)
-    # the forward pair alone against the oracle's two transforms (last mode, mode 1)
-    from paper_1809_01971_b200 import _lib
-    xs = x
-    w = torch.empty((n, n, 512), dtype=torch.float64, device="cuda")
-    _lib.call("fl_dst1_plane_pair", _lib.ptr(xs), _lib.ptr(w), 0, 1.0, _lib.stream_ptr())
-    xh = x[:3].cpu().numpy()
-    want = oracle.dst(oracle.dst(xh, axis=2), axis=1)
-    assert rel(w[:3, :, :n].cpu().numpy(), want) <= 1e-13
-
-
 @pytest.mark.parametrize("n", [7, 63, 255])
 def test_dst1_pass_layouts(n):
     """fl_dst1_pass with distinct input/output layouts vs scipy."""
