@@ -290,16 +290,70 @@ def test_svd_batched_matches_numpy(b, m, n):
 
 @pytest.mark.parametrize("b,m,n", [(4, 40, 17), (2, 64, 64), (3, 140, 130), (2, 214, 211)])
 def test_svd_batched_left_only(b, m, n):
-    """Vt = NULL (m >= n): the same rotations without the right factor, so U
-    and S are bit-identical to the full call; m < n is rejected."""
+    """Vt = NULL (m >= n): left vectors and values only.  Beyond 128 rows the
+    same rotations as the full call without the right factor (bit-identical);
+    up to 128 x 128 the half-warp-per-pair kernel (same values and vectors to
+    rounding); m < n is rejected."""
     from paper_1809_01971_b200.decomp import svd_batched
     A = torch.tensor(np.random.default_rng(b * m + n).standard_normal((b, m, n)), device="cuda")
     U, S, Vt = svd_batched(A)
     U1, S1, V1 = svd_batched(A, right=False)
-    assert V1 is None and torch.equal(U1, U) and torch.equal(S1, S)
+    assert V1 is None
+    if m > 128:
+        assert torch.equal(U1, U) and torch.equal(S1, S)
+    else:
+        assert float((S1 - S).abs().max()) <= 1e-13 * float(S.max())
+        # same left vectors up to sign
+        dots = torch.einsum("bik,bik->bk", U1, U).abs()
+        assert float((dots - 1.0).abs().max()) <= 1e-10
     if m > n:
         with pytest.raises(ValueError):
             svd_batched(A.transpose(1, 2), right=False)
+
+
+@pytest.mark.parametrize("m,n,grade", [(127, 127, 18.0), (128, 128, 0.0), (100, 60, 12.0), (65, 65, 16.0),
+                                        (127, 1, 0.0), (31, 31, 17.0)])
+def test_small_jacobi_left_sv(m, n, grade):
+    """k_jacobi_small (m, n <= 128, left vectors only) on graded, numerically
+    rank-deficient matrices like the truncation's 127-row factors: singular
+    values to 1e-13 of sigma_1 against LAPACK, U orthonormal, U diag(s) U^T
+    reproduces A A^T."""
+    from paper_1809_01971_b200.decomp import svd_batched
+    rng = np.random.default_rng(m + 7 * n)
+    k = min(m, n)
+    Q1, _ = np.linalg.qr(rng.standard_normal((m, k)))
+    Q2, _ = np.linalg.qr(rng.standard_normal((n, k)))
+    s = 10.0 ** (-grade * np.arange(k) / max(k - 1, 1))
+    A = (Q1 * s) @ Q2.T
+    U, S, _ = svd_batched(torch.tensor(A[None], device="cuda"), right=False)
+    U, S = U[0].cpu().numpy(), S[0].cpu().numpy()
+    want = np.linalg.svd(A, compute_uv=False)
+    assert np.all(np.diff(S) <= 0.0)
+    assert np.abs(S - want).max() <= 1e-13 * want[0]
+    keep = S > 1e-6 * S[0]
+    Uk = U[:, keep]
+    assert np.allclose(Uk.T @ Uk, np.eye(Uk.shape[1]), atol=1e-12)
+    assert np.linalg.norm((Uk * S[keep] ** 2) @ Uk.T - A @ A.T) <= 1e-12 * np.linalg.norm(A @ A.T)
+
+
+def test_left_sv_routes_agree():
+    """_left_sv through QR + the small Jacobi kernel (min dim <= 128) spans the
+    same leading subspace as the library SVD on a configs[1]-shaped factor."""
+    from paper_1809_01971_b200 import decomp
+    rng = np.random.default_rng(5)
+    r = 40
+    Q1, _ = np.linalg.qr(rng.standard_normal((127, 127)))
+    Q2, _ = np.linalg.qr(rng.standard_normal((2000, 127)))
+    sv = np.concatenate([np.logspace(0, -4, r), 1e-10 * np.logspace(0, -8, 127 - r)])
+    M = (Q1 * sv) @ Q2.T  # graded, leading r-subspace separated by a 1e6 gap
+    Mt = torch.tensor(M, device="cuda")
+    U1 = decomp._left_sv(Mt, r)
+    U2 = torch.linalg.svd(Mt, full_matrices=False)[0][:, :r]
+    s = np.linalg.svd(M, compute_uv=False)
+    P = U2 @ (U2.T @ U1)
+    assert float(torch.linalg.matrix_norm(P - U1)) <= 1e-9
+    sv = decomp._svdvals(Mt).cpu().numpy()
+    assert np.abs(sv - s).max() <= 1e-13 * s[0]
 
 
 def test_apply_compressed_matches_apply_then_trunc(monkeypatch):

@@ -30,12 +30,12 @@ if len(srows) > 2:
     for r in srows[2:]:
         for k in h:
             if k.startswith("stall_") and "Not Issued" not in k:
-                try: stall[k] += float(r[ix[k]])
+                try: stall[k] += float(r[ix[k]]) if ix[k] < len(r) else 0.0
                 except ValueError: pass
         op = r[ix["Source"]].split()
         if op:
             o = op[1] if op[0].startswith("@") and len(op) > 1 else op[0]
-            try: ops[o.split(".")[0]] += float(r[ix["Instructions Executed"]])
+            try: ops[o.split(".")[0]] += float(r[ix["Instructions Executed"]]) if ix["Instructions Executed"] < len(r) else 0.0
             except ValueError: pass
     S = sum(stall.values()) or 1; T = sum(ops.values()) or 1
     lines.append("== stall breakdown ==")
