@@ -189,7 +189,6 @@ __global__ void __launch_bounds__(1024) k_jacobi_small(const double* __restrict_
   __syncthreads();
   const int N = n + (n & 1);
   const int hw = threadIdx.x >> 4, l = threadIdx.x & 15;
-  const unsigned hmask = 0xffffu << (threadIdx.x & 16);  // this half warp's lanes
   const double tol = 1e-15 * (double)m, tol2 = tol * tol;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     if (threadIdx.x == 0) *flag = 0;
@@ -197,38 +196,40 @@ __global__ void __launch_bounds__(1024) k_jacobi_small(const double* __restrict_
     for (int r = 0; r < N - 1; ++r) {
       int p, q;
       rr_pair(N, r, hw, p, q);
-      if (hw < N / 2 && p < n && q < n) {
-        double* wp = W + p * JS_ROWS + l;
-        double* wq = W + q * JS_ROWS + l;
-        double x[8], y[8];
+      // every lane of every warp takes part in the reductions (full-mask
+      // shuffles; a partial mask compiles to a slow collective loop): pairs
+      // that do not exist read zeros and never rotate
+      const bool live = hw < N / 2 && p < n && q < n;
+      double* wp = W + (live ? p : 0) * JS_ROWS + l;
+      double* wq = W + (live ? q : 0) * JS_ROWS + l;
+      double x[8], y[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        x[j] = live ? wp[16 * j] : 0.0;
+        y[j] = live ? wq[16 * j] : 0.0;
+      }
+      double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        al = fma(x[j], x[j], al);
+        be = fma(y[j], y[j], be);
+        ga = fma(x[j], y[j], ga);
+      }
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) {
+        al += __shfl_xor_sync(0xffffffffu, al, o);
+        be += __shfl_xor_sync(0xffffffffu, be, o);
+        ga += __shfl_xor_sync(0xffffffffu, ga, o);
+      }
+      if (ga != 0.0 && ga * ga > tol2 * (al * be)) {
+        if (l == 0) *flag = 1;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+        const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          x[j] = wp[16 * j];
-          y[j] = wq[16 * j];
-        }
-        double al = 0.0, be = 0.0, ga = 0.0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          al = fma(x[j], x[j], al);
-          be = fma(y[j], y[j], be);
-          ga = fma(x[j], y[j], ga);
-        }
-#pragma unroll
-        for (int o = 8; o > 0; o >>= 1) {
-          al += __shfl_xor_sync(hmask, al, o);
-          be += __shfl_xor_sync(hmask, be, o);
-          ga += __shfl_xor_sync(hmask, ga, o);
-        }
-        if (ga != 0.0 && ga * ga > tol2 * (al * be)) {
-          if (l == 0) *flag = 1;
-          const double zeta = (be - al) / (2.0 * ga);
-          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-          const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            wp[16 * j] = c * x[j] - sn * y[j];
-            wq[16 * j] = sn * x[j] + c * y[j];
-          }
+          wp[16 * j] = c * x[j] - sn * y[j];
+          wq[16 * j] = sn * x[j] + c * y[j];
         }
       }
       __syncthreads();
