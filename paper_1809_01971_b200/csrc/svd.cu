@@ -166,70 +166,76 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd_jacobi(const double* __rest
 // Small-matrix fast path (m, n <= 128, m >= n, left vectors only): the
 // shapes of the truncation's factor SVDs after the QR reduction (127 x 127
 // for configs[1]).  Same one-sided Jacobi and the same convergence rule as
-// k_svd_jacobi, mapped for latency: one HALF warp per column pair (each
-// lane holds 8 rows of both columns, reductions over 16 lanes), all n/2
-// pairs of a round at once, the working matrix column-major in shared
-// memory with rows zero-padded to 128 (conflict-free 128-byte half-warp
-// accesses), the rotation test done on squares (no square root).  A round
-// costs one pair's latency chain plus one CTA barrier.
-constexpr int JS_ROWS = 128;
+// k_svd_jacobi, mapped for issue efficiency: FOUR lanes per column pair
+// (each lane holds 32 rows of both columns as 16-byte pairs), so one warp
+// runs 8 pairs and a round of all n/2 pairs is 8 warps; the per-pair scalar
+// work (reductions, rotation) is shared by 4 lanes instead of 32.  The
+// working matrix is column-major in shared memory (rows zero-padded to 128,
+// column stride 130 doubles to spread the 8 columns a warp touches over the
+// banks); the rotation test is done on squares (no square root).
+constexpr int JS_ROWS = 128, JS_LD = 130, JS_THREADS = 256;
 
-__global__ void __launch_bounds__(1024) k_jacobi_small(const double* __restrict__ A, int m, int n,
-                                                       double* __restrict__ U, double* __restrict__ S,
-                                                       int max_sweeps) {
-  extern __shared__ double sm_js[];
-  double* W = sm_js;                                         // n columns x 128 rows
-  double* sig = sm_js + (size_t)n * JS_ROWS;                 // n
-  int* flag = reinterpret_cast<int*>(sig + n);
+__global__ void __launch_bounds__(JS_THREADS, 1) k_jacobi_small(const double* __restrict__ A, int m, int n,
+                                                                double* __restrict__ U, double* __restrict__ S,
+                                                                int max_sweeps) {
+  extern __shared__ __align__(16) double sm_js[];
+  double* W = sm_js;                       // n columns x JS_LD
+  double* sig = sm_js + (size_t)n * JS_LD;  // n
+  int* flag = reinterpret_cast<int*>(sig + n + (n & 1));
   const double* Ab = A + (size_t)blockIdx.x * m * n;
-  for (int idx = threadIdx.x; idx < n * JS_ROWS; idx += blockDim.x) {
-    const int j = idx / JS_ROWS, i = idx - j * JS_ROWS;
+  for (int idx = threadIdx.x; idx < n * JS_LD; idx += blockDim.x) {
+    const int j = idx / JS_LD, i = idx - j * JS_LD;
     W[idx] = i < m ? Ab[(size_t)i * n + j] : 0.0;
   }
   __syncthreads();
   const int N = n + (n & 1);
-  const int hw = threadIdx.x >> 4, l = threadIdx.x & 15;
+  const int g = threadIdx.x >> 2, l4 = threadIdx.x & 3;
   const double tol = 1e-15 * (double)m, tol2 = tol * tol;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     if (threadIdx.x == 0) *flag = 0;
     __syncthreads();
     for (int r = 0; r < N - 1; ++r) {
       int p, q;
-      rr_pair(N, r, hw, p, q);
-      // every lane of every warp takes part in the reductions (full-mask
-      // shuffles; a partial mask compiles to a slow collective loop): pairs
+      rr_pair(N, r, g, p, q);
+      // every lane takes part in the reductions (full-mask shuffles); pairs
       // that do not exist read zeros and never rotate
-      const bool live = hw < N / 2 && p < n && q < n;
-      double* wp = W + (live ? p : 0) * JS_ROWS + l;
-      double* wq = W + (live ? q : 0) * JS_ROWS + l;
-      double x[8], y[8];
+      const bool live = g < N / 2 && p < n && q < n;
+      double2* wp = reinterpret_cast<double2*>(W + (live ? p : 0) * JS_LD) + l4;
+      double2* wq = reinterpret_cast<double2*>(W + (live ? q : 0) * JS_LD) + l4;
+      double2 x[16], y[16];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        x[j] = live ? wp[16 * j] : 0.0;
-        y[j] = live ? wq[16 * j] : 0.0;
+      for (int j = 0; j < 16; ++j) {
+        x[j] = live ? wp[4 * j] : make_double2(0.0, 0.0);
+        y[j] = live ? wq[4 * j] : make_double2(0.0, 0.0);
       }
-      double al = 0.0, be = 0.0, ga = 0.0;
+      double al = 0.0, be = 0.0, ga = 0.0, al2 = 0.0, be2 = 0.0, ga2 = 0.0;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        al = fma(x[j], x[j], al);
-        be = fma(y[j], y[j], be);
-        ga = fma(x[j], y[j], ga);
+      for (int j = 0; j < 16; ++j) {
+        al = fma(x[j].x, x[j].x, al);
+        be = fma(y[j].x, y[j].x, be);
+        ga = fma(x[j].x, y[j].x, ga);
+        al2 = fma(x[j].y, x[j].y, al2);
+        be2 = fma(y[j].y, y[j].y, be2);
+        ga2 = fma(x[j].y, y[j].y, ga2);
       }
+      al += al2;
+      be += be2;
+      ga += ga2;
 #pragma unroll
-      for (int o = 8; o > 0; o >>= 1) {
+      for (int o = 2; o > 0; o >>= 1) {
         al += __shfl_xor_sync(0xffffffffu, al, o);
         be += __shfl_xor_sync(0xffffffffu, be, o);
         ga += __shfl_xor_sync(0xffffffffu, ga, o);
       }
       if (ga != 0.0 && ga * ga > tol2 * (al * be)) {
-        if (l == 0) *flag = 1;
+        if (l4 == 0) *flag = 1;
         const double zeta = (be - al) / (2.0 * ga);
         const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
         const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          wp[16 * j] = c * x[j] - sn * y[j];
-          wq[16 * j] = sn * x[j] + c * y[j];
+        for (int j = 0; j < 16; ++j) {
+          wp[4 * j] = make_double2(c * x[j].x - sn * y[j].x, c * x[j].y - sn * y[j].y);
+          wq[4 * j] = make_double2(sn * x[j].x + c * y[j].x, sn * x[j].y + c * y[j].y);
         }
       }
       __syncthreads();
@@ -241,7 +247,7 @@ __global__ void __launch_bounds__(1024) k_jacobi_small(const double* __restrict_
   // singular values = column norms, ranked by decreasing value (ties by index)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   for (int j = warp; j < n; j += nwarps) {
-    const double* wj = W + j * JS_ROWS;
+    const double* wj = W + j * JS_LD;
     double a = 0.0;
     for (int i = lane; i < m; i += 32) a = fma(wj[i], wj[i], a);
     a = warp_sum(a);
@@ -258,7 +264,7 @@ __global__ void __launch_bounds__(1024) k_jacobi_small(const double* __restrict_
     for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
     if (lane == 0) Sb[rank] = sj;
     const double inv = sj > 0.0 ? 1.0 / sj : 0.0;
-    const double* wj = W + j * JS_ROWS;
+    const double* wj = W + j * JS_LD;
     for (int i = lane; i < m; i += 32) Ub[(size_t)i * n + rank] = (sj > 0.0) ? wj[i] * inv : (i == j ? 1.0 : 0.0);
   }
 }
@@ -287,21 +293,19 @@ int svd_batched(const double* A, int batch, int m, int n, double* U, double* S, 
 #define FL_SVD_SWEEPS 40
 #endif
   if (Vt == nullptr && m <= JS_ROWS && n <= JS_ROWS && small_svd_enabled()) {
-    const size_t smem = sizeof(double) * ((size_t)n * JS_ROWS + n) + 2 * sizeof(int);
+    const size_t smem = sizeof(double) * ((size_t)n * JS_LD + n + 1) + 2 * sizeof(int);
     static std::atomic<uint64_t> attr_js{0};
     int dev = 0;
     FL_CUDA_TRY(cudaGetDevice(&dev));
     const uint64_t bit = uint64_t(1) << (dev & 63);
     if (!(attr_js.load() & bit)) {
       FL_CUDA_TRY(cudaFuncSetAttribute(k_jacobi_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(sizeof(double) * (JS_ROWS * JS_ROWS + JS_ROWS) + 8)));
+                                       (int)(sizeof(double) * (JS_ROWS * JS_LD + JS_ROWS + 1) + 8)));
       attr_js.fetch_or(bit);
     }
-    const int N = n + (n & 1);
-    const int threads = (N / 2 * 16 + 31) / 32 * 32;
     // graded, numerically rank-deficient factors need more sweeps than random
-    // matrices (up to ~30 measured on configs[1] factors)
-    k_jacobi_small<<<batch, threads, smem, st>>>(A, m, n, U, S, 2 * FL_SVD_SWEEPS);
+    // matrices (~30 measured on configs[1] factors)
+    k_jacobi_small<<<batch, JS_THREADS, smem, st>>>(A, m, n, U, S, 2 * FL_SVD_SWEEPS);
     FL_LAUNCH_CHECK();
     return FL_OK;
   }
