@@ -205,7 +205,8 @@ int fl_col_scale(const double* U, const double* nrm, int64_t n, int64_t R,
  * F diag(P) F: b_hat = F b is the transformed right-hand side, x_hat the
  * transformed solution (x = F x_hat); r and p are N-double work arrays.
  * The whole solve is ONE cooperative persistent launch: no host round trip
- * per iteration.  hist (device, k_max + 1 doubles) receives the relative
+ * per iteration; one streaming pass (64 B/DoF) and one grid barrier per
+ * iteration.  hist (device, k_max + 1 doubles) receives the relative
  * residual history ||r_k|| / ||b||; status (device, 4 ints) receives
  * [iterations, converged, breakdown iteration, breakdown kind (1: <R,Z> <= 0,
  * 2: <P,S> <= 0)], the reference's PcgBreakdownError conditions; on a
@@ -215,15 +216,18 @@ int fl_pcg_spectral(const double* b_hat, double* x_hat, double* r, double* p,
                     int k_max, double* hist, int* status, void* stream);
 
 #define FL_PCG_WORK 8192
-/* One streaming phase of the same iteration for the slab-partitioned
- * multi-GPU solve (the caller all-reduces `out` across ranks):
- *   phase 0: x = 0, r = b, p = P b;         out = [b.b, b.Pb, p.Ap]
- *   phase 1: x += s p, r -= s A p;          out = [r.r, r.Pr]
- *   phase 2: p = P r + s p;                 out = [p.Ap]
+/* One streaming pass of the same iteration for the slab-partitioned
+ * multi-GPU solve (the caller all-reduces the 4 sums in `out` across ranks):
+ *   phase 0: x = 0, r = b, p = 0;
+ *            out = [b.b, <b, P b>, <P b, A P b>, 0]
+ *   phase 1: p = P r + beta p, x += alpha p, r -= alpha A p, z = P r;
+ *            out = [r.r, <r, z>, <z, A z>, <z, A p>]
+ * (the reference iteration with <P,S> of the next direction from
+ * <z,Az> + 2 beta' <z,Ap> + beta'^2 <p,Ap>, see fl_pcg_spectral).
  * work: FL_PCG_WORK doubles zeroed once before the first call. */
 int fl_pcg_phase(int phase, const double* b_hat, double* x_hat, double* r, double* p,
-                 const double* A, const double* P, int64_t N, double s, double* out,
-                 double* work, void* stream);
+                 const double* A, const double* P, int64_t N, double alpha, double beta,
+                 double* out, double* work, void* stream);
 
 #ifdef __cplusplus
 }

@@ -54,7 +54,7 @@ SIGNATURES = {
     "fl_col_norms": (c_int, [c_vp, c_i64, c_i64, c_vp, c_vp]),
     "fl_col_scale": (c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp]),
     "fl_pcg_spectral": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_dbl, c_int, c_vp, c_vp, c_vp]),
-    "fl_pcg_phase": (c_int, [c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp, c_vp]),
+    "fl_pcg_phase": (c_int, [c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp]),
 }
 FL_PCG_WORK = 8192
 

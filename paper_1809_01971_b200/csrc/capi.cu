@@ -236,9 +236,9 @@ int fl_pcg_spectral(const double* b_hat, double* x_hat, double* r, double* p, co
 }
 
 int fl_pcg_phase(int phase, const double* b_hat, double* x_hat, double* r, double* p, const double* A,
-                 const double* P, int64_t N, double s, double* out, double* work, void* stream) {
+                 const double* P, int64_t N, double alpha, double beta, double* out, double* work, void* stream) {
   FL_ARG_CHECK(N >= 0, "bad PCG size");
-  return pcg_phase(phase, b_hat, x_hat, r, p, A, P, N, s, out, work, as_stream(stream));
+  return pcg_phase(phase, b_hat, x_hat, r, p, A, P, N, alpha, beta, out, work, as_stream(stream));
 }
 
 }  // extern "C"

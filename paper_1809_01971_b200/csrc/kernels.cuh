@@ -68,7 +68,7 @@ int pcg_spectral(const double* b, double* x, double* r, double* p, const double*
                  double tol, int kmax, double* hist, int* status, cudaStream_t st);
 
 int pcg_phase(int which, const double* b, double* x, double* r, double* p, const double* A, const double* P,
-              int64_t N, double s, double* out, double* work, cudaStream_t st);
+              int64_t N, double alpha, double beta, double* out, double* work, cudaStream_t st);
 
 int sinc_factor(double* U, const double* mu, int64_t n, const double* t, int64_t R, double rho_min,
                 cudaStream_t st);

@@ -17,27 +17,44 @@ from paper_1809_01971_b200 import distributed as D
 
 
 class HostOps:
-    def dst_inner_modes(self, x, n1, n2):
-        if x.shape[0] == 0:
-            return x
-        z = oracle.dst(oracle.dst(x.numpy(), axis=2), axis=1)
-        return torch.from_numpy(np.ascontiguousarray(z))
+    """Host stand-in for CudaOps (oracle DSTs, numpy phases); pad > 0 adds
+    that many zero padding columns to the spectral layout, like CudaOps on
+    FFT lengths."""
+
+    def __init__(self, pad=0):
+        self.pad = pad
+
+    def pitch(self, lay):
+        return lay.dims[2] + self.pad
+
+    def dst_inner_fwd(self, x, P):
+        m, n1, n2 = x.shape
+        out = torch.zeros((m, n1, P), dtype=torch.float64)
+        if m:
+            out[..., :n2] = torch.from_numpy(oracle.dst(oracle.dst(x.numpy(), axis=2), axis=1))
+        return out
+
+    def dst_inner_bwd(self, y, n2, scale=1.0):
+        if y.shape[0] == 0:
+            return torch.zeros(y.shape[:2] + (n2,), dtype=torch.float64)
+        z = oracle.dst(oracle.dst(y.numpy()[..., :n2], axis=1), axis=2)
+        return torch.from_numpy(np.ascontiguousarray(scale * z))
 
     def dst_mode0(self, y, scale=1.0):
         if y.numel() == 0:
-            return y
+            return y.clone()
         return torch.from_numpy(np.ascontiguousarray(scale * oracle.dst(y.numpy(), axis=0)))
 
-    def pcg_phase(self, phase, b, x, r, p, A, P, s, out, work):
+    def pcg_phase(self, phase, b, x, r, p, A, P, alpha, beta, out, work):
         if phase == 0:
-            x.zero_(); r.copy_(b); p.copy_(P * b)
-            out[0], out[1], out[2] = (b * b).sum(), (b * P * b).sum(), (p * A * p).sum()
-        elif phase == 1:
-            x.add_(s * p); r.sub_(s * A * p)
-            out[0], out[1] = (r * r).sum(), (r * P * r).sum()
+            x.zero_(); r.copy_(b); p.zero_()
+            z = P * b
+            out[0], out[1], out[2], out[3] = (b * b).sum(), (b * z).sum(), (z * A * z).sum(), 0.0
         else:
-            p.mul_(s).add_(P * r)
-            out[0] = (p * A * p).sum()
+            p.mul_(beta).add_(P * r)
+            x.add_(alpha * p); r.sub_(alpha * A * p)
+            z = P * r
+            out[0], out[1], out[2], out[3] = (r * r).sum(), (r * z).sum(), (z * A * z).sum(), (z * A * p).sum()
 
     def new_work(self, like):
         return torch.zeros(8)
@@ -51,13 +68,13 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, dims, q):
+def _worker(rank, world, port, dims, q, pad=0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         lay = D.SlabLayout(dims, world, rank)
-        ops = HostOps()
+        ops = HostOps(pad)
         rng = np.random.default_rng(5)
         x_full = rng.standard_normal(dims)
         lam = [oracle.laplacian_eigenvalues(n) for n in dims]
@@ -69,12 +86,13 @@ def _worker(rank, world, port, dims, q):
         # forward transform lands in the spectral layout
         yh = D.transform_fwd(x, lay, ops)
         full_hat = oracle.transform_full(x_full)
-        err_fwd = float(np.abs(yh.numpy() - full_hat[:, ss:se, :]).max())
+        n2 = dims[2]
+        err_fwd = float(np.abs(yh.numpy()[..., :n2] - full_hat[:, ss:se, :]).max())
         back = D.transform_bwd(yh, lay, ops)
         err_rt = float(np.abs(back.numpy() - x_full[xs:xe]).max())
-        # operator application
-        A = torch.from_numpy(np.ascontiguousarray(A_full[:, ss:se, :]))
-        P = torch.from_numpy(np.ascontiguousarray(P_full[:, ss:se, :]))
+        # operator application (cores padded with zeros like the spectral layout)
+        A = D._pad_last(torch.from_numpy(np.ascontiguousarray(A_full[:, ss:se, :])), ops.pitch(lay))
+        P = D._pad_last(torch.from_numpy(np.ascontiguousarray(P_full[:, ss:se, :])), ops.pitch(lay))
         y = D.apply_slab(x, A, lay, ops, alpha=0.5)
         ya = 0.5 * oracle.apply_full(A_full, x_full)
         err_apply = float(np.abs(y.numpy() - ya[xs:xe]).max() / np.abs(ya).max())
@@ -88,12 +106,15 @@ def _worker(rank, world, port, dims, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,dims", [(2, (7, 6, 5)), (2, (8, 9, 7)), (3, (7, 5, 4))])
-def test_slab_partitioned_matches_oracle(world, dims):
+@pytest.mark.parametrize("world,dims,pad", [(2, (7, 6, 5), 0), (2, (8, 9, 7), 0), (3, (7, 5, 4), 0),
+                                            (2, (7, 6, 7), 1), (3, (7, 5, 4), 4)])
+def test_slab_partitioned_matches_oracle(world, dims, pad):
+    """Decomposition, transposes (dense and padded spectral layouts), fused
+    PCG pass protocol (one all-reduce of 4 sums per iteration) vs the oracle."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, q, pad)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]

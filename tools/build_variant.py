@@ -31,7 +31,7 @@ for src in B.sources():
         objs.append(obj)
     else:
         objs.append(os.path.join(B.BUILD, base))
-cmd = [B._nvcc()] + B.ARCH + ["-shared", "-o", out] + objs + ["-lcudart_static", "-lcublas", "-lrt", "-ldl", "-lpthread",
+cmd = [B._nvcc()] + B.ARCH + ["-shared", "-o", out] + objs + ["-lcudart_static", "-lrt", "-ldl", "-lpthread",
                                                             "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
 r = subprocess.run(cmd, capture_output=True, text=True)
 if r.returncode:
