@@ -163,7 +163,13 @@ def _solve_one(i, n, spec, max_level):
     y, cfg = problem(i, n)
     torch.cuda.current_stream().synchronize()
     t0 = time.perf_counter()
-    u, rep = solve_control_large(y, cfg, spec, max_level)
+    try:
+        u, rep = solve_control_large(y, cfg, spec, max_level)
+    except Exception as exc:  # one failed problem is recorded, the batch goes on
+        torch.cuda.current_stream().synchronize()
+        return {"problem": i, "alpha": cfg.alpha, "beta": cfg.beta, "iterations": None, "converged": False,
+                "rank": None, "seconds": time.perf_counter() - t0, "residual": None,
+                "error": "%s: %s" % (type(exc).__name__, str(exc)[:200])}
     torch.cuda.current_stream().synchronize()
     return {"problem": i, "alpha": cfg.alpha, "beta": cfg.beta, "iterations": rep.iterations,
             "converged": rep.converged, "rank": u.rank, "seconds": time.perf_counter() - t0,

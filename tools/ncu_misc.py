@@ -51,7 +51,7 @@ if "pcg" in which:
     run(); torch.cuda.synchronize()
     its = int(st[0])
     # bytes: init 5 reads/writes... count per iteration 96 B/DoF (+ init 48)
-    ev("pcg_spectral n=511 (%d its)" % its, run, nbytes=(96.0 * its + 48.0) * bh.numel())
+    ev("pcg_spectral n=511 (%d its)" % its, run, nbytes=(64.0 * its + 48.0) * bh.numel())
 if "canon" in which:
     n = 127
     spec = fl.laplacian_spectrum(n, 3)
