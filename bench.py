@@ -10,8 +10,12 @@ own tensor (independent problems, no data-path collective -> weak scaling).
 
 Extra keys: roofline of the dominant kernel (CUDA events around every launch
 of the timed region), e2e through the public API with pinned host buffers,
-cpu_baseline (numpy/scipy oracle on the host cores), clocks sampled with
-nvidia-smi during the timed region.
+cpu_baseline (numpy/scipy oracle on the host cores) and `parity` (the GPU
+apply against the oracle's result on the same tensor), clocks sampled with
+nvidia-smi during the timed region, and `solves`: configs[0] (2D full-format
+control solve), configs[1] (3D canonical, alpha 0.25/0.5/0.75), configs[3]
+(3D full format n = 1023, slab-partitioned under torchrun) and configs[4]
+(64 batched canonical problems at n = 1023, 2-problem samples at 2047..8191).
 
 `--impl reference` times the reference algorithm's CPU implementation (the
 oracle restatement of fraclap's scipy DST path) on the host cores.
@@ -534,33 +538,48 @@ def _solve_config3(args, rank, world, dev):
 
 
 def run_batch(args, rank, world, dev):
-    """BASELINE configs[4] sample: the first --batch-count problems of the
-    batch distribution at each n of --batch-n, spread over the ranks (no
-    collective on the data path); solves/s from the max-over-ranks time."""
+    """BASELINE configs[4]: the first --batch-count problems of the batch
+    distribution at each n of --batch-n (64 at n = 1023 by default, the full
+    stated batch; a 2-problem sample at the larger n, where one problem takes
+    10-35 s), spread over the ranks (no collective on the data path) and,
+    within a rank, solved --batch-conc at a time on separate CUDA streams;
+    solves/s from the max-over-ranks wall time of the whole batch."""
     import time
     import torch
     import torch.distributed as dist
     from paper_1809_01971_b200 import batch
 
+    ns = [int(v) for v in args.batch_n.split(",") if v]
+    counts = [int(v) for v in args.batch_count.split(",") if v]
+    concs = [int(v) for v in args.batch_conc.split(",") if v]
+    counts += [counts[-1]] * (len(ns) - len(counts))
+    concs += [concs[-1]] * (len(ns) - len(concs))
     per_n = {}
-    for n in [int(v) for v in args.batch_n.split(",") if v]:
+    for n, count, conc in zip(ns, counts, concs):
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
-        recs = batch.solve_batch(n, args.batch_count, rank, world)
+        recs = batch.solve_batch(n, count, rank, world, concurrency=conc)
         torch.cuda.synchronize()
         t = time.perf_counter() - t0
         if world > 1:
             tt = torch.tensor([t], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t = float(tt)
-        per_n[str(n)] = {"problems": args.batch_count, "seconds": t, "solves_per_s": args.batch_count / t,
-                         "rank0_records": [{"alpha": round(r["alpha"], 4), "beta": r["beta"],
+        ok = sum(1 for r in recs if r["converged"])
+        per_n[str(n)] = {"problems": count, "concurrency_per_gpu": conc, "seconds": t, "solves_per_s": count / t,
+                         "rank0_converged": ok, "rank0_solved": len(recs),
+                         "rank0_iterations": [r["iterations"] for r in recs],
+                         "rank0_records": [{"problem": r["problem"], "alpha": round(r["alpha"], 4), "beta": r["beta"],
                                             "iterations": r["iterations"], "converged": r["converged"],
-                                            "rank": r["rank"], "seconds": round(r["seconds"], 3)} for r in recs]}
+                                            "rank": r["rank"], "seconds": round(r["seconds"], 3),
+                                            **({"error": r["error"]} if r.get("error") else {})} for r in recs]}
         torch.cuda.empty_cache()
     return {"per_n": per_n, "n_gpus": world,
             "path": "canonical PCG per problem (exp-sum control core, ladder preconditioner <= 1023 "
-                    "interpolated in log eigenvalue, range-compressed truncation), problems spread over ranks"}
+                    "interpolated in log eigenvalue, range-compressed truncation), problems spread over ranks, "
+                    "several per GPU on separate streams (library factorizations serialised)"}
 
 
 def main(argv=None):
@@ -575,7 +594,8 @@ def main(argv=None):
     p.add_argument("--solve-n", type=int, default=1023)
     p.add_argument("--no-batch", action="store_true", help="skip the configs[4] batch sample")
     p.add_argument("--batch-n", default="1023,2047,4095,8191")
-    p.add_argument("--batch-count", type=int, default=1)
+    p.add_argument("--batch-count", default="64,2,2,2", help="problems per n (comma list, last repeats)")
+    p.add_argument("--batch-conc", default="4,2,2,2", help="concurrent problems per GPU per n")
     args = p.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3

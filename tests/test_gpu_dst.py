@@ -44,11 +44,16 @@ def test_dst_apply_api(n):
     m = spectral.laplacian_mode(n)
     rng = np.random.default_rng(n)
     X = rng.standard_normal((n, 5))
-    got = spectral.dst_apply(m, X).cpu().numpy()
+    got = spectral.dst_apply(m, X)
+    assert isinstance(got, np.ndarray)  # numpy in -> numpy out, like the reference
     assert rel(got, oracle.dst(X, axis=0)) <= 1e-13
     v = rng.standard_normal(n)
-    back = spectral.dst_apply(m, spectral.dst_apply(m, v), "inverse").cpu().numpy()
+    back = spectral.dst_apply(m, spectral.dst_apply(m, v), "inverse")
     assert rel(back, v) <= 1e-13
+    Xt = torch.tensor(X, device="cuda")
+    gt = spectral.dst_apply(m, Xt)
+    assert isinstance(gt, torch.Tensor) and gt.is_cuda  # device tensors stay on the device
+    assert rel(gt.cpu().numpy(), oracle.dst(X, axis=0)) <= 1e-13
     with pytest.raises(ValueError):
         spectral.dst_apply(m, np.zeros(n + 1))
     with pytest.raises(ValueError):
