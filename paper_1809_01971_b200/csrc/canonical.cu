@@ -106,21 +106,28 @@ int col_norms(const double* U, int64_t n, int64_t R, double* out, cudaStream_t s
 
 // out[c] scaled columns: V[r][c] = U[r][c] / nrm[c] (nrm == 0 -> e_1 column)
 // V may alias U (in-place normalisation): every element is read and written
-// by the same thread
+// by the same thread.  Threads run along the columns (R fastest, coalesced),
+// blocks stride over the rows: no 64-bit division per element; the divide
+// (not a reciprocal multiply) keeps the reference's rounding of U / nrm.
 __global__ void k_col_scale(const double* U, const double* __restrict__ nrm, int64_t n, int64_t R, double* V) {
-  const int64_t total = n * R;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / R, c = i % R;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < R; c += (int64_t)gridDim.x * blockDim.x) {
     const double s = nrm[c];
-    V[i] = (s == 0.0) ? (r == 0 ? 1.0 : 0.0) : U[i] / s;
+    for (int64_t r = blockIdx.y; r < n; r += gridDim.y) {
+      const int64_t i = r * R + c;
+      V[i] = (s == 0.0) ? (r == 0 ? 1.0 : 0.0) : U[i] / s;
+    }
   }
 }
 
 int col_scale(const double* U, const double* nrm, int64_t n, int64_t R, double* V, cudaStream_t st) {
   if (n * R <= 0) return FL_OK;
-  int64_t g = (n * R + 255) / 256;
-  if (g > (int64_t)sm_count() * 8) g = (int64_t)sm_count() * 8;
-  k_col_scale<<<(unsigned)g, 256, 0, st>>>(U, nrm, n, R, V);
+  int64_t gx = (R + 255) / 256;
+  if (gx > 65535) gx = 65535;
+  int64_t gy = ((int64_t)sm_count() * 8 + gx - 1) / gx;
+  if (gy > n) gy = n;
+  if (gy > 65535) gy = 65535;
+  if (gy < 1) gy = 1;
+  k_col_scale<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, st>>>(U, nrm, n, R, V);
   FL_LAUNCH_CHECK();
   return FL_OK;
 }

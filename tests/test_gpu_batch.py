@@ -33,3 +33,35 @@ def test_coarse_preconditioner_and_batch_solve():
     P = fl.cp_to_dense(batch.preconditioner_coarse(kind, spec, 6, max_level=31)).cpu().numpy()
     inv = 1.0 / oracle.dense_core("g2", [oracle.laplacian_eigenvalues(n)] * 3, 0.5, 1e-2, 1e2)
     assert np.linalg.norm(P - inv) <= 5e-2 * np.linalg.norm(inv)
+
+
+@pytest.mark.parametrize("i", [0, 1, 2, 3])
+def test_large_grid_route_matches_reference_route(i):
+    """configs[4]'s large-n route (exp-sum system core, ladder preconditioner
+    stopped at a coarse level and interpolated in log eigenvalue) against the
+    reference-shaped route (solve_control: multigrid-Tucker cores, the full
+    ladder; the reference's own algorithm, solver.py:203-216) on the SAME
+    problem of the configs[4] distribution at n = 63, and both against the
+    exact optimality solve: the two routes must land on the same solution to
+    the accuracy the PCG tolerance and eps = 1e-6 allow."""
+    n = 63
+    spec = fl.laplacian_spectrum(n, 3)
+    y, cfg = batch.problem(i, n)
+    u_big, rep_big = batch.solve_control_large(y, cfg, spec, max_level=31)
+    u_ref, rep_ref = fl.solve_control(y, cfg, spec)
+    assert rep_big.converged and rep_ref.converged
+    yd = fl.cp_to_dense(y)
+    yd = yd.cpu().numpy() if isinstance(yd, torch.Tensor) else np.asarray(yd)
+    _, u_exact = oracle.kkt_dense_solve(yd, cfg.alpha, cfg.beta, cfg.gamma)
+
+    def dense(u):
+        d = fl.cp_to_dense(u)
+        return d.cpu().numpy() if isinstance(d, torch.Tensor) else np.asarray(d)
+
+    a, b = dense(u_big), dense(u_ref)
+    e_big = np.linalg.norm(a - u_exact) / np.linalg.norm(u_exact)
+    e_ref = np.linalg.norm(b - u_exact) / np.linalg.norm(u_exact)
+    e_ab = np.linalg.norm(a - b) / np.linalg.norm(b)
+    print("problem %d alpha %.3f beta %.2e: its %d / %d, err vs exact %.2e / %.2e, routes %.2e"
+          % (i, cfg.alpha, cfg.beta, rep_big.iterations, rep_ref.iterations, e_big, e_ref, e_ab))
+    assert e_big <= 1e-4 and e_ref <= 1e-4 and e_ab <= 2e-4
