@@ -173,11 +173,15 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd_jacobi(const double* __rest
 // working matrix is column-major in shared memory (rows zero-padded to 128,
 // column stride 130 doubles to spread the 8 columns a warp touches over the
 // banks); the rotation test is done on squares (no square root).
-constexpr int JS_ROWS = 128, JS_LD = 130, JS_THREADS = 256;
+constexpr int JS_ROWS = 128, JS_THREADS = 256;
 
+// ROWS: working rows (m <= ROWS, zero-padded), 32 / 64 / 128 -> each lane
+// holds ROWS / 4 rows of both columns of its pair
+template <int ROWS>
 __global__ void __launch_bounds__(JS_THREADS, 1) k_jacobi_small(const double* __restrict__ A, int m, int n,
                                                                 double* __restrict__ U, double* __restrict__ S,
                                                                 int max_sweeps) {
+  constexpr int JS_LD = ROWS + 2, NJ = ROWS / 8;  // NJ: double2 per lane and column
   extern __shared__ __align__(16) double sm_js[];
   double* W = sm_js;                       // n columns x JS_LD
   double* sig = sm_js + (size_t)n * JS_LD;  // n
@@ -202,15 +206,15 @@ __global__ void __launch_bounds__(JS_THREADS, 1) k_jacobi_small(const double* __
       const bool live = g < N / 2 && p < n && q < n;
       double2* wp = reinterpret_cast<double2*>(W + (live ? p : 0) * JS_LD) + l4;
       double2* wq = reinterpret_cast<double2*>(W + (live ? q : 0) * JS_LD) + l4;
-      double2 x[16], y[16];
+      double2 x[NJ], y[NJ];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
+      for (int j = 0; j < NJ; ++j) {
         x[j] = live ? wp[4 * j] : make_double2(0.0, 0.0);
         y[j] = live ? wq[4 * j] : make_double2(0.0, 0.0);
       }
       double al = 0.0, be = 0.0, ga = 0.0, al2 = 0.0, be2 = 0.0, ga2 = 0.0;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
+      for (int j = 0; j < NJ; ++j) {
         al = fma(x[j].x, x[j].x, al);
         be = fma(y[j].x, y[j].x, be);
         ga = fma(x[j].x, y[j].x, ga);
@@ -233,7 +237,7 @@ __global__ void __launch_bounds__(JS_THREADS, 1) k_jacobi_small(const double* __
         const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
         const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < NJ; ++j) {
           wp[4 * j] = make_double2(c * x[j].x - sn * y[j].x, c * x[j].y - sn * y[j].y);
           wq[4 * j] = make_double2(sn * x[j].x + c * y[j].x, sn * x[j].y + c * y[j].y);
         }
@@ -273,6 +277,25 @@ __global__ void __launch_bounds__(JS_THREADS, 1) k_jacobi_small(const double* __
 
 constexpr size_t SVD_SMEM_CAP = 200 * 1024;
 
+template <int ROWS>
+static int launch_jacobi_small(const double* A, int batch, int m, int n, double* U, double* S, int sweeps,
+                               cudaStream_t st) {
+  constexpr int LD = ROWS + 2;
+  const size_t smem = sizeof(double) * ((size_t)n * LD + n + 1) + 2 * sizeof(int);
+  static std::atomic<uint64_t> attr_js{0};
+  int dev = 0;
+  FL_CUDA_TRY(cudaGetDevice(&dev));
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  if (!(attr_js.load() & bit)) {
+    FL_CUDA_TRY(cudaFuncSetAttribute(k_jacobi_small<ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(sizeof(double) * (JS_ROWS * LD + JS_ROWS + 1) + 8)));
+    attr_js.fetch_or(bit);
+  }
+  k_jacobi_small<ROWS><<<batch, JS_THREADS, smem, st>>>(A, m, n, U, S, sweeps);
+  FL_LAUNCH_CHECK();
+  return FL_OK;
+}
+
 static bool small_svd_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -293,21 +316,11 @@ int svd_batched(const double* A, int batch, int m, int n, double* U, double* S, 
 #define FL_SVD_SWEEPS 40
 #endif
   if (Vt == nullptr && m <= JS_ROWS && n <= JS_ROWS && small_svd_enabled()) {
-    const size_t smem = sizeof(double) * ((size_t)n * JS_LD + n + 1) + 2 * sizeof(int);
-    static std::atomic<uint64_t> attr_js{0};
-    int dev = 0;
-    FL_CUDA_TRY(cudaGetDevice(&dev));
-    const uint64_t bit = uint64_t(1) << (dev & 63);
-    if (!(attr_js.load() & bit)) {
-      FL_CUDA_TRY(cudaFuncSetAttribute(k_jacobi_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(sizeof(double) * (JS_ROWS * JS_LD + JS_ROWS + 1) + 8)));
-      attr_js.fetch_or(bit);
-    }
     // graded, numerically rank-deficient factors need more sweeps than random
     // matrices (~30 measured on configs[1] factors)
-    k_jacobi_small<<<batch, JS_THREADS, smem, st>>>(A, m, n, U, S, 2 * FL_SVD_SWEEPS);
-    FL_LAUNCH_CHECK();
-    return FL_OK;
+    if (m <= 32) return launch_jacobi_small<32>(A, batch, m, n, U, S, 2 * FL_SVD_SWEEPS, st);
+    if (m <= 64) return launch_jacobi_small<64>(A, batch, m, n, U, S, 2 * FL_SVD_SWEEPS, st);
+    return launch_jacobi_small<128>(A, batch, m, n, U, S, 2 * FL_SVD_SWEEPS, st);
   }
   int w_sm = 0, v_sm = 0;
   if (wb + vb + tail <= SVD_SMEM_CAP) {
