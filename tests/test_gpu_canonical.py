@@ -380,14 +380,16 @@ def test_apply_compressed_matches_apply_then_trunc(monkeypatch):
     assert got.rank == want.rank
     # both truncations are within the tolerance of the untruncated product;
     # terms at the cutoff may be chosen differently under different rounding
-    nd = fl.cp_norm(dense)
-    e_got = fl.cp_norm(fl.cp_add(got, fl.cp_scale(dense, -1.0))) / nd
-    e_want = fl.cp_norm(fl.cp_add(want, fl.cp_scale(dense, -1.0))) / nd
-    e_diff = fl.cp_norm(fl.cp_add(got, fl.cp_scale(want, -1.0))) / nd
+    # differences measured on the dense 127^3 expansions: a canonical
+    # difference norm through Gram products cannot resolve relative
+    # differences below ~sqrt(eps) = 1.5e-8 (cancellation in |a|^2 + |b|^2 - 2<a,b>)
+    from paper_1809_01971_b200.full import cp_dense
+    Dp, Dg, Dw = cp_dense(dense), cp_dense(got), cp_dense(want)
+    nd = float(torch.linalg.vector_norm(Dp))
+    e_got = float(torch.linalg.vector_norm(Dg - Dp)) / nd
+    e_want = float(torch.linalg.vector_norm(Dw - Dp)) / nd
+    e_diff = float(torch.linalg.vector_norm(Dg - Dw)) / nd
     print("trunc errors vs the product: compressed %.2e, reference-shaped %.2e, difference %.2e"
           % (e_got, e_want, e_diff))
-    assert e_got <= 1e-8
-    # the reference-shaped truncation may overshoot its nominal tolerance: c2t's
-    # rank-growth test compares a rounding-level difference (decomp.py:402-438)
-    assert e_want <= 3e-8
-    assert e_diff <= 1.01 * (e_got + e_want)
+    assert e_got <= 1e-8 and e_want <= 1e-8
+    assert e_diff <= 1.01 * (e_got + e_want) + 1e-13
