@@ -1,0 +1,81 @@
+"""Size-independent checks at BASELINE.json's FULL config sizes, where the
+CPU oracle cannot run the whole problem: every solver output is verified
+against the control equation of the reference (solver.py:203-216),
+(beta A^-alpha + (gamma/beta) A^alpha) u = y_design, evaluated through an
+independent code path (the dense full-format apply, F diag(g2) F, on the
+register-resident DST kernels)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1809_01971_b200 as fl
+from paper_1809_01971_b200 import batch, full, fullsolve
+from paper_1809_01971_b200.full import cp_dense
+
+pytestmark = pytest.mark.gpu
+
+
+def _control_residual(spec, cfg, u_dense, y_dense):
+    kind = fl.CoreFunctionKind("g2", cfg.alpha, coeff_minus=float(cfg.beta),
+                               coeff_plus=float(cfg.gamma) / float(cfg.beta))
+    op = full.FullOperator.from_kind(kind, spec)
+    r = op(u_dense.contiguous())
+    r.sub_(y_dense)
+    return float(torch.linalg.vector_norm(r) / torch.linalg.vector_norm(y_dense))
+
+
+def test_config3_full_size_control_equation():
+    """configs[3] at its stated size (n = 1023, alpha 0.75, beta 1e-4, 16 bumps
+    + 1e-3 noise, rank-6 Kronecker preconditioner, tol 1e-8): the returned
+    control satisfies the control equation to the PCG tolerance when the
+    operator is re-applied in nodal form (5-pass apply, not the spectral
+    recurrence that produced it)."""
+    n = 1023
+    spec = fl.laplacian_spectrum(n, 3)
+    cfg = fl.SolverConfig(alpha=0.75, beta=1e-4, precond_rank=6, residual_tol=1e-8, k_max=100)
+    y = cp_dense(fl.gaussian_bumps(n, 3, 16, seed=7))
+    g = torch.Generator(device="cuda")
+    g.manual_seed(77)
+    y.add_(1e-3 * torch.randn(y.shape, dtype=torch.float64, device="cuda", generator=g))
+    u, rep = fullsolve.solve_control_full(y, cfg, spec)
+    assert rep.converged
+    res = _control_residual(spec, cfg, u, y)
+    print("configs[3] n=1023: %d its, reported %.3e, re-applied residual %.3e" % (rep.iterations,
+                                                                                 rep.residuals[-1], res))
+    assert res <= 1.5e-8
+    assert abs(res - rep.residuals[-1]) <= 1e-9
+
+
+@pytest.mark.parametrize("alpha", [0.25, 0.5, 0.75])
+def test_config1_full_size_control_equation(alpha):
+    """configs[1] at its stated size (n = 127, beta 1e-2, eps 1e-8, tol 1e-6):
+    the truncated canonical solve's control, expanded densely, satisfies the
+    control equation to the PCG tolerance (the iteration's residuals are
+    truncated-arithmetic estimates; this re-applies the exact operator)."""
+    n = 127
+    spec = fl.laplacian_spectrum(n, 3)
+    y = fl.gaussian_bumps(n, 3, 8, seed=11)
+    cfg = fl.SolverConfig(alpha=alpha, beta=1e-2, eps=1e-8, precond_rank=6, residual_tol=1e-6, k_max=60)
+    u, rep = fl.solve_control(y, cfg, spec)
+    assert rep.converged
+    res = _control_residual(spec, cfg, cp_dense(u), cp_dense(y))
+    print("configs[1] n=127 alpha %.2f: %d its, reported %.3e, re-applied %.3e" % (alpha, rep.iterations,
+                                                                                   rep.residuals[-1], res))
+    assert res <= 2e-6
+
+
+@pytest.mark.parametrize("i", [0, 1])
+def test_config4_full_size_control_equation(i):
+    """configs[4] at n = 1023 (problems 0 and 1 of the 64-problem batch,
+    eps 1e-6, tol 1e-6): the large-grid route's control, expanded densely
+    (8.6 GB), satisfies the exact control equation to the PCG tolerance."""
+    n = 1023
+    spec = fl.laplacian_spectrum(n, 3)
+    y, cfg = batch.problem(i, n)
+    u, rep = batch.solve_control_large(y, cfg, spec)
+    assert rep.converged
+    res = _control_residual(spec, cfg, cp_dense(u), cp_dense(y))
+    print("configs[4] n=1023 problem %d: %d its, reported %.3e, re-applied %.3e" % (i, rep.iterations,
+                                                                                    rep.residuals[-1], res))
+    assert res <= 1e-5
