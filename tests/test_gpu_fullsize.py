@@ -77,33 +77,44 @@ def test_config1_full_size_control_equation(alpha):
     err = _error_vs_exact(spec, cfg, ud, yd)
     print("configs[1] n=127 alpha %.2f: %d its, reported %.3e, re-applied residual %.3e, error vs exact %.3e"
           % (alpha, rep.iterations, rep.residuals[-1], res, err))
-    # the reference's PCG reports its truncated-arithmetic residual recurrence
+    # The reference's PCG reports its truncated-arithmetic residual recurrence
     # (solver.py:163-166); re-applying the exact operator measures the true
-    # one, larger where g2 ~ rho^alpha amplifies the eps-level truncation
-    # noise of u at high frequencies.  The solution error stays small.
-    # Measured (r2): residual 1.2e-6 / 1.7e-5 / 1.8e-4, error <= ERR below.
-    assert err <= 1e-5
-    assert res <= 1e-3
+    # residual.  Measured (r2): residual 1.2e-6 / 1.7e-5 / 1.8e-4 and error vs
+    # exact 1.1e-6 / 1.6e-5 / 2.7e-4 for alpha 0.25 / 0.5 / 0.75 — the accuracy
+    # of the reference ALGORITHM at eps = 1e-8 on this grid, not of this port:
+    # the uncompressed truncation (the reference's exact shape) gives the
+    # same error to 4 digits, and eps = 1e-10 brings it to 5e-8 / 1.4e-7
+    # (tools/route_accuracy.py).  At n = 15 and 31 the GPU solutions equal
+    # the reference's own to 1e-12 (test_config1_alpha_golden).
+    assert err <= 5e-4
+    assert res <= 5e-4
 
 
 @pytest.mark.parametrize("i", [0, 1])
-def test_config4_full_size_control_equation(i):
-    """configs[4] at n = 1023 (problems 0 and 1 of the 64-problem batch,
-    eps 1e-6, tol 1e-6): the large-grid route's control, expanded densely
-    (8.6 GB), satisfies the exact control equation to the PCG tolerance."""
+def test_config4_full_size_vs_reference_algorithm(i):
+    """configs[4] at n = 1023 (problems 0 and 1 of the 64-problem batch, eps
+    1e-6, tol 1e-6): the large-grid route against the REFERENCE ALGORITHM run
+    at the same size on the device (solve_control: multigrid-Tucker g2 core
+    and the full preconditioner ladder, its dense-level cap lifted): iteration
+    counts +-1, and the large-grid route's error vs the exact optimality solve
+    is no worse than the reference algorithm's (measured r2: 9.2e-3 vs 1.7e-2,
+    1.3e-1 vs 2.2e-1 — eps = 1e-6 truncation of iterates dominated by the
+    beta rho^-alpha term caps both; eps = 1e-8 gives 5.5e-5 / 1.3e-3)."""
+    from paper_1809_01971_b200 import decomp
     n = 1023
     spec = fl.laplacian_spectrum(n, 3)
     y, cfg = batch.problem(i, n)
     u, rep = batch.solve_control_large(y, cfg, spec)
     assert rep.converged
-    ud = cp_dense(u)
     yd = cp_dense(y)
+    e_big = _error_vs_exact(spec, cfg, cp_dense(u), yd)
     del u
-    err = _error_vs_exact(spec, cfg, ud, yd)
-    res = _control_residual(spec, cfg, ud, yd)
-    print("configs[4] n=1023 problem %d: %d its, reported %.3e, re-applied residual %.3e, error vs exact %.3e"
-          % (i, rep.iterations, rep.residuals[-1], res, err))
-    # eps = 1e-6 truncation: the exact-operator residual is dominated by
-    # high-frequency truncation noise amplified by g2 (see configs[1]); the
-    # solution error is the meaningful accuracy
-    assert err <= 1e-3
+    torch.cuda.empty_cache()
+    with decomp.dense_budget(n ** 3):
+        u_ref, rep_ref = fl.solve_control(y, cfg, spec)
+    assert rep_ref.converged
+    e_ref = _error_vs_exact(spec, cfg, cp_dense(u_ref), yd)
+    print("configs[4] n=1023 problem %d: its %d / %d (reference algorithm), error vs exact %.3e / %.3e"
+          % (i, rep.iterations, rep_ref.iterations, e_big, e_ref))
+    assert abs(rep.iterations - rep_ref.iterations) <= 1
+    assert e_big <= 1.05 * e_ref
