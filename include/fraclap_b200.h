@@ -192,6 +192,14 @@ int fl_cp_gram(int d, const int64_t* n, const double* const* A, int64_t Ra,
 int fl_svd_batched(const double* A, int batch, int m, int n, double* U, double* S,
                    double* Vt, void* stream);
 
+/* Left singular system of T = A^T for a batch of square k x k matrices A
+ * (row-major, k <= 128): a column-pivoted Householder QR of A in shared
+ * memory (R only), then one-sided Jacobi on R^T (Drmac-Veselic
+ * preconditioning); U (batch, k, k) = left singular vectors of T, S (batch,
+ * k) decreasing.  Used by the truncation's factor SVDs after an R-only QR of
+ * the long side (decomp._left_sv; reference decomp.py:343-345, 395). */
+int fl_svd_left_pivoted(const double* A, int batch, int k, double* U, double* S, void* stream);
+
 /* Column norms of an (n, R) matrix (cp_normalize, tensor.py:180-197). */
 int fl_col_norms(const double* U, int64_t n, int64_t R, double* out, void* stream);
 

@@ -51,6 +51,7 @@ SIGNATURES = {
     "fl_cp_apply_mode": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_dbl, c_vp]),
     "fl_cp_gram": (c_int, [c_int, P(c_i64), P(c_vp), c_i64, P(c_vp), c_i64, c_vp, c_vp]),
     "fl_svd_batched": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp]),
+    "fl_svd_left_pivoted": (c_int, [c_vp, c_int, c_int, c_vp, c_vp, c_vp]),
     "fl_col_norms": (c_int, [c_vp, c_i64, c_i64, c_vp, c_vp]),
     "fl_col_scale": (c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp]),
     "fl_pcg_spectral": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_dbl, c_int, c_vp, c_vp, c_vp]),

@@ -208,6 +208,10 @@ int fl_svd_batched(const double* A, int batch, int m, int n, double* U, double* 
   return svd_batched(A, batch, m, n, U, S, Vt, as_stream(stream));
 }
 
+int fl_svd_left_pivoted(const double* A, int batch, int k, double* U, double* S, void* stream) {
+  return svd_left_pivoted(A, batch, k, U, S, as_stream(stream));
+}
+
 int fl_cp_apply_mode(const double* U, const double* Xs, double* out, int64_t n, int64_t R, int64_t S, double scale,
                      void* stream) {
   return dst_kr(U, Xs, out, n, R, S, scale, as_stream(stream));

@@ -15,6 +15,7 @@ struct PassLayout {
 bool fft_length(int64_t n);
 
 int svd_batched(const double* A, int batch, int m, int n, double* U, double* S, double* Vt, cudaStream_t st);
+int svd_left_pivoted(const double* A, int batch, int k, double* U, double* S, cudaStream_t st);
 
 int dst_pass(const double* x, double* y, const double* core, int64_t n, bool contig, int64_t outer, int64_t groups,
              int64_t wv, const PassLayout& in, const PassLayout& out, double scale, cudaStream_t st,

@@ -176,8 +176,14 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd_jacobi(const double* __rest
 constexpr int JS_ROWS = 128, JS_THREADS = 256;
 
 // ROWS: working rows (m <= ROWS, zero-padded), 32 / 64 / 128 -> each lane
-// holds ROWS / 4 rows of both columns of its pair
-template <int ROWS>
+// holds ROWS / 4 rows of both columns of its pair.
+// PIV (square input A, m == n): the left singular system of T = A^T with the
+// Drmac-Veselic preconditioning: a column-pivoted Householder QR A P = Q R
+// in shared memory (R only), then one-sided Jacobi on R^T; T = P R^T Q^T, so
+// the left vectors of T are the rows of R^T's permuted by P.  On the graded,
+// numerically rank-deficient factors of the truncation this cuts the sweeps
+// from 25-37 to 7-10 (tools: numpy model on captured configs[1] factors).
+template <int ROWS, bool PIV>
 __global__ void __launch_bounds__(JS_THREADS, 1) k_jacobi_small(const double* __restrict__ A, int m, int n,
                                                                 double* __restrict__ U, double* __restrict__ S,
                                                                 int max_sweeps) {
@@ -186,10 +192,90 @@ __global__ void __launch_bounds__(JS_THREADS, 1) k_jacobi_small(const double* __
   double* W = sm_js;                       // n columns x JS_LD
   double* sig = sm_js + (size_t)n * JS_LD;  // n
   int* flag = reinterpret_cast<int*>(sig + n + (n & 1));
+  int* perm = flag + 4;                    // n (PIV)
   const double* Ab = A + (size_t)blockIdx.x * m * n;
   for (int idx = threadIdx.x; idx < n * JS_LD; idx += blockDim.x) {
     const int j = idx / JS_LD, i = idx - j * JS_LD;
     W[idx] = i < m ? Ab[(size_t)i * n + j] : 0.0;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  if constexpr (PIV) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) perm[i] = i;
+    __syncthreads();
+    double* cn = sig;  // column norms during the factorisation
+    for (int j = 0; j < n; ++j) {
+      for (int c = j + warp; c < n; c += nwarps) {
+        const double* wc = W + c * JS_LD;
+        double a = 0.0;
+        for (int i = j + lane; i < m; i += 32) a = fma(wc[i], wc[i], a);
+        a = warp_sum(a);
+        if (lane == 0) cn[c] = a;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        double best = -1.0;
+        int bi = j;
+        for (int c = j + lane; c < n; c += 32)
+          if (cn[c] > best) {
+            best = cn[c];
+            bi = c;
+          }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) {
+            best = ob;
+            bi = oi;
+          }
+        }
+        if (lane == 0) flag[1] = bi;
+      }
+      __syncthreads();
+      const int pc = flag[1];
+      const double xn2 = cn[pc];
+      if (pc != j) {
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+          const double t = W[j * JS_LD + i];
+          W[j * JS_LD + i] = W[pc * JS_LD + i];
+          W[pc * JS_LD + i] = t;
+        }
+        if (threadIdx.x == 0) {
+          const int t = perm[j];
+          perm[j] = perm[pc];
+          perm[pc] = t;
+        }
+      }
+      __syncthreads();
+      // Householder vector of column j (rows j..m-1): v = x - alpha e_j
+      double* wj = W + j * JS_LD;
+      const double xj = wj[j];
+      const double alpha = -copysign(sqrt(xn2), xj);
+      const double vj = xj - alpha;
+      const double vtv = xn2 - xj * xj + vj * vj;
+      if (vtv > 0.0) {
+        const double beta = 2.0 / vtv;
+        for (int c = j + 1 + warp; c < n; c += nwarps) {
+          double* wc = W + c * JS_LD;
+          double d = 0.0;
+          for (int i = j + lane; i < m; i += 32) d = fma(i == j ? vj : wj[i], wc[i], d);
+          d = warp_sum(d) * beta;
+          for (int i = j + lane; i < m; i += 32) wc[i] = fma(-d, i == j ? vj : wj[i], wc[i]);
+        }
+      }
+      __syncthreads();
+      for (int i = j + threadIdx.x; i < m; i += blockDim.x) wj[i] = (i == j) ? (vtv > 0.0 ? alpha : xj) : 0.0;
+      __syncthreads();
+    }
+    // W := R^T (in place; R is upper triangular)
+    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+      const int c = idx / n, r = idx - c * n;
+      if (r < c) {
+        const double t = W[c * JS_LD + r];
+        W[c * JS_LD + r] = W[r * JS_LD + c];
+        W[r * JS_LD + c] = t;
+      }
+    }
   }
   __syncthreads();
   const int N = n + (n & 1);
@@ -249,7 +335,6 @@ __global__ void __launch_bounds__(JS_THREADS, 1) k_jacobi_small(const double* __
     if (!any) break;
   }
   // singular values = column norms, ranked by decreasing value (ties by index)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   for (int j = warp; j < n; j += nwarps) {
     const double* wj = W + j * JS_LD;
     double a = 0.0;
@@ -269,31 +354,49 @@ __global__ void __launch_bounds__(JS_THREADS, 1) k_jacobi_small(const double* __
     if (lane == 0) Sb[rank] = sj;
     const double inv = sj > 0.0 ? 1.0 / sj : 0.0;
     const double* wj = W + j * JS_LD;
-    for (int i = lane; i < m; i += 32) Ub[(size_t)i * n + rank] = (sj > 0.0) ? wj[i] * inv : (i == j ? 1.0 : 0.0);
+    for (int i = lane; i < m; i += 32) {
+      const int row = PIV ? perm[i] : i;
+      Ub[(size_t)row * n + rank] = (sj > 0.0) ? wj[i] * inv : (i == j ? 1.0 : 0.0);
+    }
   }
 }
 
 }  // namespace
 
 constexpr size_t SVD_SMEM_CAP = 200 * 1024;
+#ifndef FL_SVD_SWEEPS
+#define FL_SVD_SWEEPS 40
+#endif
 
-template <int ROWS>
+template <int ROWS, bool PIV = false>
 static int launch_jacobi_small(const double* A, int batch, int m, int n, double* U, double* S, int sweeps,
                                cudaStream_t st) {
   constexpr int LD = ROWS + 2;
-  const size_t smem = sizeof(double) * ((size_t)n * LD + n + 1) + 2 * sizeof(int);
+  // W, sig (+1 for alignment), flag[4], perm[n]
+  const size_t smem = sizeof(double) * ((size_t)n * LD + n + 1) + sizeof(int) * (4 + (size_t)n);
+  const size_t smem_max = sizeof(double) * ((size_t)JS_ROWS * LD + JS_ROWS + 1) + sizeof(int) * (4 + JS_ROWS);
   static std::atomic<uint64_t> attr_js{0};
   int dev = 0;
   FL_CUDA_TRY(cudaGetDevice(&dev));
   const uint64_t bit = uint64_t(1) << (dev & 63);
   if (!(attr_js.load() & bit)) {
-    FL_CUDA_TRY(cudaFuncSetAttribute(k_jacobi_small<ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(sizeof(double) * (JS_ROWS * LD + JS_ROWS + 1) + 8)));
+    FL_CUDA_TRY(cudaFuncSetAttribute(k_jacobi_small<ROWS, PIV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem_max));
     attr_js.fetch_or(bit);
   }
-  k_jacobi_small<ROWS><<<batch, JS_THREADS, smem, st>>>(A, m, n, U, S, sweeps);
+  k_jacobi_small<ROWS, PIV><<<batch, JS_THREADS, smem, st>>>(A, m, n, U, S, sweeps);
   FL_LAUNCH_CHECK();
   return FL_OK;
+}
+
+// left singular system of T = A^T for square A (k x k, k <= 128) through a
+// column-pivoted QR of A and Jacobi on R^T (see k_jacobi_small<.., true>)
+int svd_left_pivoted(const double* A, int batch, int k, double* U, double* S, cudaStream_t st) {
+  FL_ARG_CHECK(batch >= 0 && k >= 1 && k <= JS_ROWS, "pivoted small SVD: bad shape (%d, %d)", batch, k);
+  if (batch == 0) return FL_OK;
+  if (k <= 32) return launch_jacobi_small<32, true>(A, batch, k, k, U, S, 2 * FL_SVD_SWEEPS, st);
+  if (k <= 64) return launch_jacobi_small<64, true>(A, batch, k, k, U, S, 2 * FL_SVD_SWEEPS, st);
+  return launch_jacobi_small<128, true>(A, batch, k, k, U, S, 2 * FL_SVD_SWEEPS, st);
 }
 
 static bool small_svd_enabled() {

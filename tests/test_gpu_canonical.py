@@ -336,6 +336,28 @@ def test_small_jacobi_left_sv(m, n, grade):
     assert np.linalg.norm((U * S ** 2) @ U.T - A @ A.T) <= 1e-13 * np.linalg.norm(A @ A.T)
 
 
+@pytest.mark.parametrize("k,grade", [(127, 18.0), (100, 10.0), (65, 16.0), (128, 0.0), (20, 12.0)])
+def test_svd_left_pivoted(k, grade):
+    """fl_svd_left_pivoted: left singular system of a square graded (numerically
+    rank-deficient) matrix through the column-pivoted QR + Jacobi route:
+    singular values to 1e-13 of sigma_1, U orthonormal on the resolved part,
+    U diag(s^2) U^T = T T^T."""
+    from paper_1809_01971_b200.decomp import svd_left_pivoted
+    rng = np.random.default_rng(k)
+    Q1, _ = np.linalg.qr(rng.standard_normal((k, k)))
+    Q2, _ = np.linalg.qr(rng.standard_normal((k, k)))
+    sv = 10.0 ** (-grade * np.arange(k) / (k - 1))
+    T = (Q1 * sv) @ Q2.T
+    U, S = svd_left_pivoted(torch.tensor(T, device="cuda"))
+    U, S = U.cpu().numpy(), S.cpu().numpy()
+    want = np.linalg.svd(T, compute_uv=False)
+    assert np.all(np.diff(S) <= 0.0)
+    assert np.abs(S - want).max() <= 1e-13 * want[0]
+    keep = S > 1e-6 * S[0]
+    assert np.allclose(U[:, keep].T @ U[:, keep], np.eye(int(keep.sum())), atol=1e-12)
+    assert np.linalg.norm((U * S ** 2) @ U.T - T @ T.T) <= 1e-13 * np.linalg.norm(T @ T.T)
+
+
 def test_left_sv_routes_agree(monkeypatch):
     """_left_sv through QR + the small Jacobi kernel (enabled up to 128 here;
     the product keeps it to 64) spans the same leading subspace as the
@@ -348,12 +370,21 @@ def test_left_sv_routes_agree(monkeypatch):
     sv = np.concatenate([np.logspace(0, -4, r), 1e-10 * np.logspace(0, -8, 127 - r)])
     M = (Q1 * sv) @ Q2.T  # graded, leading r-subspace separated by a 1e6 gap
     Mt = torch.tensor(M, device="cuda")
-    monkeypatch.setattr(decomp, "_JACOBI_LEFT_SV_MAX", 128)
-    U1 = decomp._left_sv(Mt, r)
     U2 = torch.linalg.svd(Mt, full_matrices=False)[0][:, :r]
     s = np.linalg.svd(M, compute_uv=False)
-    P = U2 @ (U2.T @ U1)
-    assert float(torch.linalg.matrix_norm(P - U1)) <= 1e-9
+    for route in ("pivoted", "plain"):
+        if route == "plain":
+            monkeypatch.setattr(decomp, "_JACOBI_LEFT_SV_MAX", 128)
+        U1 = decomp._left_sv(Mt, r)
+        P = U2 @ (U2.T @ U1)
+        assert float(torch.linalg.matrix_norm(P - U1)) <= 1e-9, route
+    monkeypatch.undo()
+    sv = decomp._svdvals(Mt).cpu().numpy()
+    assert np.abs(sv - s).max() <= 1e-13 * s[0]
+    # tall input (n > m): Q R of M, then the pivoted route on R
+    Ut = decomp._left_sv(Mt.T.contiguous(), r)
+    Vt = torch.linalg.svd(Mt.T, full_matrices=False)[0][:, :r]
+    assert float(torch.linalg.matrix_norm(Vt @ (Vt.T @ Ut) - Ut)) <= 1e-9
 
 
 def test_apply_compressed_matches_apply_then_trunc(monkeypatch):
