@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(JS_THREADS, 1) k_jacobi_small(const double* __
   double* sig = sm_js + (size_t)n * JS_LD;  // n
   int* flag = reinterpret_cast<int*>(sig + n + (n & 1));
   int* perm = flag + 4;                    // n (PIV)
+  int* lastmod = perm + n;                 // n: global round of each column's last rotation
   const double* Ab = A + (size_t)blockIdx.x * m * n;
   for (int idx = threadIdx.x; idx < n * JS_LD; idx += blockDim.x) {
     const int j = idx / JS_LD, i = idx - j * JS_LD;
@@ -277,6 +278,7 @@ __global__ void __launch_bounds__(JS_THREADS, 1) k_jacobi_small(const double* __
       }
     }
   }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) lastmod[i] = -(1 << 30);
   __syncthreads();
   const int N = n + (n & 1);
   const int g = threadIdx.x >> 2, l4 = threadIdx.x & 3;
@@ -288,8 +290,13 @@ __global__ void __launch_bounds__(JS_THREADS, 1) k_jacobi_small(const double* __
       int p, q;
       rr_pair(N, r, g, p, q);
       // every lane takes part in the reductions (full-mask shuffles); pairs
-      // that do not exist read zeros and never rotate
-      const bool live = g < N / 2 && p < n && q < n;
+      // that do not exist read zeros and never rotate.  A pair found
+      // converged one sweep ago (N - 1 rounds, the round-robin period) whose
+      // columns have not been rotated since is still converged: skipped
+      // without reading its columns (the late sweeps touch few pairs).
+      const int gr = sweep * (N - 1) + r;
+      bool live = g < N / 2 && p < n && q < n;
+      if (live && sweep > 0 && lastmod[p] < gr - (N - 1) && lastmod[q] < gr - (N - 1)) live = false;
       double2* wp = reinterpret_cast<double2*>(W + (live ? p : 0) * JS_LD) + l4;
       double2* wq = reinterpret_cast<double2*>(W + (live ? q : 0) * JS_LD) + l4;
       double2 x[NJ], y[NJ];
@@ -318,7 +325,11 @@ __global__ void __launch_bounds__(JS_THREADS, 1) k_jacobi_small(const double* __
         ga += __shfl_xor_sync(0xffffffffu, ga, o);
       }
       if (ga != 0.0 && ga * ga > tol2 * (al * be)) {
-        if (l4 == 0) *flag = 1;
+        if (l4 == 0) {
+          *flag = 1;
+          lastmod[p] = gr;
+          lastmod[q] = gr;
+        }
         const double zeta = (be - al) / (2.0 * ga);
         const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
         const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
@@ -372,9 +383,9 @@ template <int ROWS, bool PIV = false>
 static int launch_jacobi_small(const double* A, int batch, int m, int n, double* U, double* S, int sweeps,
                                cudaStream_t st) {
   constexpr int LD = ROWS + 2;
-  // W, sig (+1 for alignment), flag[4], perm[n]
-  const size_t smem = sizeof(double) * ((size_t)n * LD + n + 1) + sizeof(int) * (4 + (size_t)n);
-  const size_t smem_max = sizeof(double) * ((size_t)JS_ROWS * LD + JS_ROWS + 1) + sizeof(int) * (4 + JS_ROWS);
+  // W, sig (+1 for alignment), flag[4], perm[n], lastmod[n]
+  const size_t smem = sizeof(double) * ((size_t)n * LD + n + 1) + sizeof(int) * (4 + 2 * (size_t)n);
+  const size_t smem_max = sizeof(double) * ((size_t)JS_ROWS * LD + JS_ROWS + 1) + sizeof(int) * (4 + 2 * JS_ROWS);
   static std::atomic<uint64_t> attr_js{0};
   int dev = 0;
   FL_CUDA_TRY(cudaGetDevice(&dev));

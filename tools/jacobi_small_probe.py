@@ -31,3 +31,14 @@ if os.path.exists(p):
         tm("real %s jacobi on R^T" % (tuple(M.shape),), lambda: decomp.svd_batched(X[None], right=False))
         tm("real %s _left_sv" % (tuple(M.shape),), lambda: decomp._left_sv(M, 40))
         tm("real %s lib svd" % (tuple(M.shape),), lambda: torch.linalg.svd(M, full_matrices=False))
+# pivoted route (column-pivoted QR + Jacobi on R^T)
+for k in (64, 127):
+    Q1, _ = np.linalg.qr(rng.standard_normal((k, k))); Q2, _ = np.linalg.qr(rng.standard_normal((k, k)))
+    G = torch.tensor((Q1 * 10.0 ** (-18 * np.arange(k) / (k - 1))) @ Q2.T, device="cuda")
+    tm("pivoted graded 1e-18 %dx%d" % (k, k), lambda: decomp.svd_left_pivoted(G))
+if os.path.exists(p):
+    for key in d.files[:3]:
+        M = torch.tensor(d[key], device="cuda")
+        R = torch.linalg.qr(M.T, mode="r")[1]
+        tm("real %s pivoted on R^T" % (tuple(M.shape),), lambda: decomp.svd_left_pivoted(R.T))
+        tm("real %s _left_sv (pivoted route)" % (tuple(M.shape),), lambda: decomp._left_sv(M, 40))
