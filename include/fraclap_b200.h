@@ -200,6 +200,32 @@ int fl_svd_batched(const double* A, int batch, int m, int n, double* U, double* 
  * the long side (decomp._left_sv; reference decomp.py:343-345, 395). */
 int fl_svd_left_pivoted(const double* A, int batch, int k, double* U, double* S, void* stream);
 
+/* Limits of the batched wide-matrix factorisations below. */
+#define FL_QR_MAX_BATCH 8
+#define FL_QR_MAX_K 128
+#define FL_QR_MAX_LEAVES 256
+
+/* R factors of tall-skinny QR factorisations, hand-written TSQR (Householder
+ * leaves in shared memory, pairwise merges of the triangles): for each of
+ * batch <= FL_QR_MAX_BATCH wide matrices M_i (k_i x m_i, 1 <= k_i <=
+ * FL_QR_MAX_K, element (r, c) at M_i[r * rs_i + c * cs_i], one of the two
+ * strides equal to 1 for coalesced reads) R_i (k_i x k_i row-major, upper
+ * triangular, zeros below) with M_i^T = Q R_i.  M, k, m, rs, cs, R are host
+ * arrays of length batch.  Replaces the library geqrf in the truncation's
+ * factor SVDs (decomp.py:343-345, 373, 395) and in the range finder. */
+int fl_qr_r(int batch, const double* const* M, const int* k, const int64_t* m,
+            const int64_t* rs, const int64_t* cs, double* const* R, void* stream);
+
+/* Left singular systems of the same kind of batch: fl_qr_r followed by the
+ * pivoted one-CTA Jacobi of fl_svd_left_pivoted on every R_i^T, all matrices
+ * in one launch each (the three mode factors of rhosvd / _pick_ranks,
+ * decomp.py:343-345, 373, run concurrently).  U_i (k_i x k_i row-major,
+ * columns = left singular vectors of M_i) and S_i (k_i, decreasing); U may be
+ * NULL, or hold NULL entries, for singular values only. */
+int fl_left_sv_wide(int batch, const double* const* M, const int* k, const int64_t* m,
+                    const int64_t* rs, const int64_t* cs, double* const* U,
+                    double* const* S, void* stream);
+
 /* Column norms of an (n, R) matrix (cp_normalize, tensor.py:180-197). */
 int fl_col_norms(const double* U, int64_t n, int64_t R, double* out, void* stream);
 

@@ -41,6 +41,9 @@ void set_error(const char* fmt, ...);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// raise the default memory pool's release threshold (once per device)
+int keep_pool_cached();
+
 // stream-ordered device temporary, freed on every exit path
 struct DevBuf {
   double* p = nullptr;
@@ -50,6 +53,7 @@ struct DevBuf {
   DevBuf& operator=(const DevBuf&) = delete;
   int alloc(int64_t count, cudaStream_t s) {
     st = s;
+    if (int rc = keep_pool_cached()) return rc;
     FL_CUDA_TRY(cudaMallocAsync(&p, sizeof(double) * (size_t)count, s));
     return FL_OK;
   }

@@ -16,6 +16,10 @@ bool fft_length(int64_t n);
 
 int svd_batched(const double* A, int batch, int m, int n, double* U, double* S, double* Vt, cudaStream_t st);
 int svd_left_pivoted(const double* A, int batch, int k, double* U, double* S, cudaStream_t st);
+int tsqr_r(int batch, const double* const* M, const int* k, const int64_t* m, const int64_t* rs, const int64_t* cs,
+           double* const* R, cudaStream_t st);
+int left_sv_wide(int batch, const double* const* M, const int* k, const int64_t* m, const int64_t* rs,
+                 const int64_t* cs, double* const* U, double* const* S, cudaStream_t st);
 
 int dst_pass(const double* x, double* y, const double* core, int64_t n, bool contig, int64_t outer, int64_t groups,
              int64_t wv, const PassLayout& in, const PassLayout& out, double scale, cudaStream_t st,

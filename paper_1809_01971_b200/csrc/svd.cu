@@ -183,10 +183,11 @@ constexpr int JS_ROWS = 128, JS_THREADS = 256;
 // the left vectors of T are the rows of R^T's permuted by P.  On the graded,
 // numerically rank-deficient factors of the truncation this cuts the sweeps
 // from 25-37 to 7-10 (tools: numpy model on captured configs[1] factors).
+// Ab: one m x n row-major matrix; Ub (m x n, may be null: values only), Sb (n)
 template <int ROWS, bool PIV>
-__global__ void __launch_bounds__(JS_THREADS, 1) k_jacobi_small(const double* __restrict__ A, int m, int n,
-                                                                double* __restrict__ U, double* __restrict__ S,
-                                                                int max_sweeps) {
+__device__ __forceinline__ void jacobi_small_body(const double* __restrict__ Ab, int m, int n,
+                                                  double* __restrict__ Ub, double* __restrict__ Sb,
+                                                  int max_sweeps) {
   constexpr int JS_LD = ROWS + 2, NJ = ROWS / 8;  // NJ: double2 per lane and column
   extern __shared__ __align__(16) double sm_js[];
   double* W = sm_js;                       // n columns x JS_LD
@@ -194,7 +195,6 @@ __global__ void __launch_bounds__(JS_THREADS, 1) k_jacobi_small(const double* __
   int* flag = reinterpret_cast<int*>(sig + n + (n & 1));
   int* perm = flag + 4;                    // n (PIV)
   int* lastmod = perm + n;                 // n: global round of each column's last rotation
-  const double* Ab = A + (size_t)blockIdx.x * m * n;
   for (int idx = threadIdx.x; idx < n * JS_LD; idx += blockDim.x) {
     const int j = idx / JS_LD, i = idx - j * JS_LD;
     W[idx] = i < m ? Ab[(size_t)i * n + j] : 0.0;
@@ -354,8 +354,6 @@ __global__ void __launch_bounds__(JS_THREADS, 1) k_jacobi_small(const double* __
     if (lane == 0) sig[j] = sqrt(a);
   }
   __syncthreads();
-  double* Ub = U + (size_t)blockIdx.x * m * n;
-  double* Sb = S + (size_t)blockIdx.x * n;
   for (int j = warp; j < n; j += nwarps) {
     const double sj = sig[j];
     int rank = 0;
@@ -363,6 +361,7 @@ __global__ void __launch_bounds__(JS_THREADS, 1) k_jacobi_small(const double* __
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
     if (lane == 0) Sb[rank] = sj;
+    if (Ub == nullptr) continue;
     const double inv = sj > 0.0 ? 1.0 / sj : 0.0;
     const double* wj = W + j * JS_LD;
     for (int i = lane; i < m; i += 32) {
@@ -370,6 +369,33 @@ __global__ void __launch_bounds__(JS_THREADS, 1) k_jacobi_small(const double* __
       Ub[(size_t)row * n + rank] = (sj > 0.0) ? wj[i] * inv : (i == j ? 1.0 : 0.0);
     }
   }
+}
+
+template <int ROWS, bool PIV>
+__global__ void __launch_bounds__(JS_THREADS, 1) k_jacobi_small(const double* __restrict__ A, int m, int n,
+                                                                double* __restrict__ U, double* __restrict__ S,
+                                                                int max_sweeps) {
+  jacobi_small_body<ROWS, PIV>(A + (size_t)blockIdx.x * m * n, m, n, U + (size_t)blockIdx.x * m * n,
+                               S + (size_t)blockIdx.x * n, max_sweeps);
+}
+
+// Pivoted small SVDs of square matrices of different sizes in one launch:
+// CTA i takes the k_i x k_i matrix A_i (the R factors of tsqr_r).
+struct JacobiMulti {
+  const double* A[FL_QR_MAX_BATCH];
+  double* U[FL_QR_MAX_BATCH];
+  double* S[FL_QR_MAX_BATCH];
+  int k[FL_QR_MAX_BATCH];
+};
+
+__global__ void __launch_bounds__(JS_THREADS, 1) k_jacobi_multi(const JacobiMulti jm, int max_sweeps) {
+  const int i = blockIdx.x, k = jm.k[i];
+  if (k <= 32)
+    jacobi_small_body<32, true>(jm.A[i], k, k, jm.U[i], jm.S[i], max_sweeps);
+  else if (k <= 64)
+    jacobi_small_body<64, true>(jm.A[i], k, k, jm.U[i], jm.S[i], max_sweeps);
+  else
+    jacobi_small_body<128, true>(jm.A[i], k, k, jm.U[i], jm.S[i], max_sweeps);
 }
 
 }  // namespace
@@ -410,6 +436,51 @@ int svd_left_pivoted(const double* A, int batch, int k, double* U, double* S, cu
   return launch_jacobi_small<128, true>(A, batch, k, k, U, S, 2 * FL_SVD_SWEEPS, st);
 }
 
+// Left singular systems of a batch of wide matrices M_i (k_i x m_i, k_i <=
+// 128): R_i of M_i^T = Q R by TSQR (qr.cu), then the pivoted Jacobi on every
+// R_i in one launch.  U_i may be null (singular values only).
+int left_sv_wide(int batch, const double* const* M, const int* k, const int64_t* m, const int64_t* rs,
+                 const int64_t* cs, double* const* U, double* const* S, cudaStream_t st) {
+  FL_ARG_CHECK(batch >= 0 && batch <= FL_QR_MAX_BATCH, "left_sv_wide: batch must be 0..%d", FL_QR_MAX_BATCH);
+  if (batch == 0) return FL_OK;
+  size_t total = 0, off[FL_QR_MAX_BATCH];
+  int kmax = 1;
+  for (int i = 0; i < batch; ++i) {
+    FL_ARG_CHECK(k[i] >= 1 && k[i] <= JS_ROWS, "left_sv_wide: k = %d outside 1..%d", k[i], JS_ROWS);
+    FL_ARG_CHECK(S[i] != nullptr, "left_sv_wide: null output");
+    off[i] = total;
+    total += (size_t)k[i] * k[i];
+    if (k[i] > kmax) kmax = k[i];
+  }
+  DevBuf rbuf;
+  int rc = rbuf.alloc((int64_t)total, st);
+  if (rc) return rc;
+  double* R[FL_QR_MAX_BATCH];
+  for (int i = 0; i < batch; ++i) R[i] = rbuf.p + off[i];
+  if ((rc = tsqr_r(batch, M, k, m, rs, cs, R, st))) return rc;
+  JacobiMulti jm{};
+  for (int i = 0; i < batch; ++i) {
+    jm.A[i] = R[i];
+    jm.U[i] = U ? U[i] : nullptr;
+    jm.S[i] = S[i];
+    jm.k[i] = k[i];
+  }
+  const int rows = kmax <= 32 ? 32 : kmax <= 64 ? 64 : 128;
+  const size_t smem = sizeof(double) * ((size_t)kmax * (rows + 2) + kmax + 1) + sizeof(int) * (4 + 2 * (size_t)kmax);
+  const size_t smem_max = sizeof(double) * ((size_t)JS_ROWS * (JS_ROWS + 2) + JS_ROWS + 1) + sizeof(int) * (4 + 2 * JS_ROWS);
+  static std::atomic<uint64_t> attr_jm{0};
+  int dev = 0;
+  FL_CUDA_TRY(cudaGetDevice(&dev));
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  if (!(attr_jm.load() & bit)) {
+    FL_CUDA_TRY(cudaFuncSetAttribute(k_jacobi_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
+    attr_jm.fetch_or(bit);
+  }
+  k_jacobi_multi<<<batch, JS_THREADS, smem, st>>>(jm, 2 * FL_SVD_SWEEPS);
+  FL_LAUNCH_CHECK();
+  return FL_OK;
+}
+
 static bool small_svd_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -446,6 +517,9 @@ int svd_batched(const double* A, int batch, int m, int n, double* U, double* S, 
   double* scratch = nullptr;
   // per-matrix scratch stride, the same one the kernel indexes with
   const size_t gstride = M * K + (Vt ? K * K : 0);
+  if (!(w_sm && v_sm)) {
+    if (int rc = keep_pool_cached()) return rc;
+  }
   if (!(w_sm && v_sm)) FL_CUDA_TRY(cudaMallocAsync(&scratch, sizeof(double) * gstride * (size_t)batch, st));
   // function attributes are per device: one flag bit per device ordinal
   static std::atomic<uint64_t> attr_set{0};
