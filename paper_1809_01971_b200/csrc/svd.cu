@@ -166,14 +166,20 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd_jacobi(const double* __rest
 // Small-matrix fast path (m, n <= 128, m >= n, left vectors only): the
 // shapes of the truncation's factor SVDs after the QR reduction (127 x 127
 // for configs[1]).  Same one-sided Jacobi and the same convergence rule as
-// k_svd_jacobi, mapped for issue efficiency: FOUR lanes per column pair
-// (each lane holds 32 rows of both columns as 16-byte pairs), so one warp
-// runs 8 pairs and a round of all n/2 pairs is 8 warps; the per-pair scalar
-// work (reductions, rotation) is shared by 4 lanes instead of 32.  The
+// k_svd_jacobi, mapped for issue efficiency: JS_LPP (8) lanes per column
+// pair (each lane holds ROWS / 8 rows of both columns as 16-byte pairs), so
+// one warp runs 4 pairs and a round of all n/2 pairs is up to 16 warps; the
+// per-pair scalar work (reductions, rotation) is shared by 8 lanes instead
+// of 32.  (Four lanes per pair, 8 warps: the rounds are latency-bound and
+// ran ~1.4x longer, tools/jsmall_var.py.)  The
 // working matrix is column-major in shared memory (rows zero-padded to 128,
 // column stride 130 doubles to spread the 8 columns a warp touches over the
 // banks); the rotation test is done on squares (no square root).
-constexpr int JS_ROWS = 128, JS_THREADS = 256;
+#ifndef FL_JS_LPP
+#define FL_JS_LPP 8
+#endif
+// LPP lanes per column pair; 64 pairs (128 columns) per round
+constexpr int JS_ROWS = 128, JS_LPP = FL_JS_LPP, JS_THREADS = 64 * JS_LPP;
 
 // ROWS: working rows (m <= ROWS, zero-padded), 32 / 64 / 128 -> each lane
 // holds ROWS / 4 rows of both columns of its pair.
@@ -188,7 +194,8 @@ template <int ROWS, bool PIV>
 __device__ __forceinline__ void jacobi_small_body(const double* __restrict__ Ab, int m, int n,
                                                   double* __restrict__ Ub, double* __restrict__ Sb,
                                                   int max_sweeps) {
-  constexpr int JS_LD = ROWS + 2, NJ = ROWS / 8;  // NJ: double2 per lane and column
+  constexpr int JS_LD = ROWS + 2, NJ = ROWS / (2 * JS_LPP);  // NJ: double2 per lane and column
+  static_assert(NJ * 2 * JS_LPP == ROWS, "rows must split over the lanes of a pair");
   extern __shared__ __align__(16) double sm_js[];
   double* W = sm_js;                       // n columns x JS_LD
   double* sig = sm_js + (size_t)n * JS_LD;  // n
@@ -281,7 +288,7 @@ __device__ __forceinline__ void jacobi_small_body(const double* __restrict__ Ab,
   for (int i = threadIdx.x; i < n; i += blockDim.x) lastmod[i] = -(1 << 30);
   __syncthreads();
   const int N = n + (n & 1);
-  const int g = threadIdx.x >> 2, l4 = threadIdx.x & 3;
+  const int g = threadIdx.x / JS_LPP, l4 = threadIdx.x % JS_LPP;
   const double tol = 1e-15 * (double)m, tol2 = tol * tol;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     if (threadIdx.x == 0) *flag = 0;
@@ -302,8 +309,8 @@ __device__ __forceinline__ void jacobi_small_body(const double* __restrict__ Ab,
       double2 x[NJ], y[NJ];
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {
-        x[j] = live ? wp[4 * j] : make_double2(0.0, 0.0);
-        y[j] = live ? wq[4 * j] : make_double2(0.0, 0.0);
+        x[j] = live ? wp[JS_LPP * j] : make_double2(0.0, 0.0);
+        y[j] = live ? wq[JS_LPP * j] : make_double2(0.0, 0.0);
       }
       double al = 0.0, be = 0.0, ga = 0.0, al2 = 0.0, be2 = 0.0, ga2 = 0.0;
 #pragma unroll
@@ -319,7 +326,7 @@ __device__ __forceinline__ void jacobi_small_body(const double* __restrict__ Ab,
       be += be2;
       ga += ga2;
 #pragma unroll
-      for (int o = 2; o > 0; o >>= 1) {
+      for (int o = JS_LPP / 2; o > 0; o >>= 1) {
         al += __shfl_xor_sync(0xffffffffu, al, o);
         be += __shfl_xor_sync(0xffffffffu, be, o);
         ga += __shfl_xor_sync(0xffffffffu, ga, o);
@@ -335,8 +342,8 @@ __device__ __forceinline__ void jacobi_small_body(const double* __restrict__ Ab,
         const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
-          wp[4 * j] = make_double2(c * x[j].x - sn * y[j].x, c * x[j].y - sn * y[j].y);
-          wq[4 * j] = make_double2(sn * x[j].x + c * y[j].x, sn * x[j].y + c * y[j].y);
+          wp[JS_LPP * j] = make_double2(c * x[j].x - sn * y[j].x, c * x[j].y - sn * y[j].y);
+          wq[JS_LPP * j] = make_double2(sn * x[j].x + c * y[j].x, sn * x[j].y + c * y[j].y);
         }
       }
       __syncthreads();
@@ -394,6 +401,8 @@ __global__ void __launch_bounds__(JS_THREADS, 1) k_jacobi_multi(const JacobiMult
     jacobi_small_body<32, true>(jm.A[i], k, k, jm.U[i], jm.S[i], max_sweeps);
   else if (k <= 64)
     jacobi_small_body<64, true>(jm.A[i], k, k, jm.U[i], jm.S[i], max_sweeps);
+  else if (k <= 96)
+    jacobi_small_body<96, true>(jm.A[i], k, k, jm.U[i], jm.S[i], max_sweeps);
   else
     jacobi_small_body<128, true>(jm.A[i], k, k, jm.U[i], jm.S[i], max_sweeps);
 }
@@ -433,6 +442,7 @@ int svd_left_pivoted(const double* A, int batch, int k, double* U, double* S, cu
   if (batch == 0) return FL_OK;
   if (k <= 32) return launch_jacobi_small<32, true>(A, batch, k, k, U, S, 2 * FL_SVD_SWEEPS, st);
   if (k <= 64) return launch_jacobi_small<64, true>(A, batch, k, k, U, S, 2 * FL_SVD_SWEEPS, st);
+  if (k <= 96) return launch_jacobi_small<96, true>(A, batch, k, k, U, S, 2 * FL_SVD_SWEEPS, st);
   return launch_jacobi_small<128, true>(A, batch, k, k, U, S, 2 * FL_SVD_SWEEPS, st);
 }
 
@@ -465,7 +475,7 @@ int left_sv_wide(int batch, const double* const* M, const int* k, const int64_t*
     jm.S[i] = S[i];
     jm.k[i] = k[i];
   }
-  const int rows = kmax <= 32 ? 32 : kmax <= 64 ? 64 : 128;
+  const int rows = kmax <= 32 ? 32 : kmax <= 64 ? 64 : kmax <= 96 ? 96 : 128;
   const size_t smem = sizeof(double) * ((size_t)kmax * (rows + 2) + kmax + 1) + sizeof(int) * (4 + 2 * (size_t)kmax);
   const size_t smem_max = sizeof(double) * ((size_t)JS_ROWS * (JS_ROWS + 2) + JS_ROWS + 1) + sizeof(int) * (4 + 2 * JS_ROWS);
   static std::atomic<uint64_t> attr_jm{0};
@@ -505,6 +515,7 @@ int svd_batched(const double* A, int batch, int m, int n, double* U, double* S, 
     // matrices (~30 measured on configs[1] factors)
     if (m <= 32) return launch_jacobi_small<32>(A, batch, m, n, U, S, 2 * FL_SVD_SWEEPS, st);
     if (m <= 64) return launch_jacobi_small<64>(A, batch, m, n, U, S, 2 * FL_SVD_SWEEPS, st);
+    if (m <= 96) return launch_jacobi_small<96>(A, batch, m, n, U, S, 2 * FL_SVD_SWEEPS, st);
     return launch_jacobi_small<128>(A, batch, m, n, U, S, 2 * FL_SVD_SWEEPS, st);
   }
   int w_sm = 0, v_sm = 0;
