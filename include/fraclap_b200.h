@@ -200,6 +200,17 @@ int fl_svd_batched(const double* A, int batch, int m, int n, double* U, double* 
  * the long side (decomp._left_sv; reference decomp.py:343-345, 395). */
 int fl_svd_left_pivoted(const double* A, int batch, int k, double* U, double* S, void* stream);
 
+/* Khatri-Rao contraction on the FP64 tensor cores (hand-written DMMA GEMM
+ * whose A operand is generated while loading, reduction split over R with a
+ * fixed-order second pass): out[(ia, ib), j] = sum_r Pa[ia, r] Pb[ib, r]
+ * Y[r, j].  Pa (a x R) and Pb (b x R) row-major contiguous; Y element (r, j)
+ * at Y[r * sYr + j * sYj]; out (a*b x N) row-major contiguous.  The ALS
+ * matrices U_l (KR(Pa, Pb) diag(xi))^T of canonical-to-Tucker and the core
+ * projection (decomp.py:349-353, 384-399). */
+int fl_kr_contract(const double* Pa, int64_t a, const double* Pb, int64_t b, int64_t R,
+                   const double* Y, int64_t sYr, int64_t sYj, int64_t N, double* out,
+                   void* stream);
+
 /* Limits of the batched wide-matrix factorisations below. */
 #define FL_QR_MAX_BATCH 8
 #define FL_QR_MAX_K 128

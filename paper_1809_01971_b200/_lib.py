@@ -52,6 +52,7 @@ SIGNATURES = {
     "fl_cp_gram": (c_int, [c_int, P(c_i64), P(c_vp), c_i64, P(c_vp), c_i64, c_vp, c_vp]),
     "fl_svd_batched": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp]),
     "fl_svd_left_pivoted": (c_int, [c_vp, c_int, c_int, c_vp, c_vp, c_vp]),
+    "fl_kr_contract": (c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),
     "fl_qr_r": (c_int, [c_int, P(c_vp), P(c_int), P(c_i64), P(c_i64), P(c_i64), P(c_vp), c_vp]),
     "fl_left_sv_wide": (c_int, [c_int, P(c_vp), P(c_int), P(c_i64), P(c_i64), P(c_i64), P(c_vp), P(c_vp), c_vp]),
     "fl_col_norms": (c_int, [c_vp, c_i64, c_i64, c_vp, c_vp]),

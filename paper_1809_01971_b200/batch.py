@@ -176,7 +176,7 @@ def _solve_one(i, n, spec, max_level):
             "residual": rep.residuals[-1]}
 
 
-def solve_batch(n, count, rank=0, world=1, max_level=1023, concurrency=1, serial_linalg=True):
+def solve_batch(n, count, rank=0, world=1, max_level=1023, concurrency=1, serial_linalg=True, indices=None):
     """Solve problems rank, rank+world, ... of the batch; returns per-problem
     records (in problem order).
 
@@ -185,10 +185,11 @@ def solve_batch(n, count, rank=0, world=1, max_level=1023, concurrency=1, serial
     chain of small, latency-bound steps (factor SVDs, Gram products, kept-rank
     decisions on the host) that leaves most of the B200 idle, so independent
     problems overlap almost perfectly.  Every problem's arithmetic is the same
-    as in a sequential run (same kernels, same order of operations)."""
+    as in a sequential run (same kernels, same order of operations).
+    `indices` selects explicit problem numbers instead of this rank's share."""
     from .spectral import laplacian_spectrum
     spec = laplacian_spectrum(n, 3)
-    idx = problem_indices(count, rank, world)
+    idx = list(indices) if indices is not None else problem_indices(count, rank, world)
     if concurrency <= 1 or len(idx) <= 1:
         return [_solve_one(i, n, spec, max_level) for i in idx]
     dev = torch.cuda.current_device()

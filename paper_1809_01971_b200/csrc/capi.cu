@@ -233,6 +233,11 @@ int fl_svd_left_pivoted(const double* A, int batch, int k, double* U, double* S,
   return svd_left_pivoted(A, batch, k, U, S, as_stream(stream));
 }
 
+int fl_kr_contract(const double* Pa, int64_t a, const double* Pb, int64_t b, int64_t R, const double* Y,
+                   int64_t sYr, int64_t sYj, int64_t N, double* out, void* stream) {
+  return kr_contract(Pa, a, Pb, b, R, Y, sYr, sYj, N, out, as_stream(stream));
+}
+
 int fl_qr_r(int batch, const double* const* M, const int* k, const int64_t* m, const int64_t* rs, const int64_t* cs,
             double* const* R, void* stream) {
   FL_ARG_CHECK(batch == 0 || (M && k && m && rs && cs && R), "fl_qr_r: null argument array");

@@ -52,6 +52,11 @@ int gemm_f64(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int
              int64_t bA, const double* B, int64_t sBk, int64_t sBn, int64_t bB, double beta, double* C,
              int64_t sCm, int64_t sCn, int64_t bC, int64_t batch, cudaStream_t st);
 
+// out[(ia, ib), j] = sum_r Pa[ia, r] Pb[ib, r] Y[r, j] (kr_contract.cu); Pa (a x R), Pb (b x R) row-major,
+// Y element (r, j) at Y[r * sYr + j * sYj], out (a b x N) row-major
+int kr_contract(const double* Pa, int64_t a, const double* Pb, int64_t b, int64_t R, const double* Y, int64_t sYr,
+                int64_t sYj, int64_t N, double* out, cudaStream_t st);
+
 int ew_mul(const double* a, const double* b, double* out, int64_t count, double scale, cudaStream_t st);
 
 int kr_expand(const double* U, const double* Xs, double* out, int64_t n, int64_t R, int64_t S, cudaStream_t st);

@@ -444,6 +444,29 @@ def test_left_sv_wide_rejects_bad_shapes():
         _lib.call("fl_qr_r", 9, ptrs, ks, ms, rs, cs, ptrs, _lib.stream_ptr())
 
 
+@pytest.mark.parametrize("a,b,R,N,ymajor", [(40, 37, 5000, 127, "r"), (40, 37, 5000, 127, "j"), (64, 64, 4096, 64, "r"),
+                                          (3, 5, 17, 2, "j"), (50, 51, 100001, 61, "r"), (7, 1, 300, 200, "j"),
+                                          (1, 1, 1, 1, "r"), (33, 31, 255, 129, "r")])
+def test_kr_contract(a, b, R, N, ymajor):
+    """fl_kr_contract (fused Khatri-Rao DMMA GEMM, split reduction) against
+    the explicit Khatri-Rao product; deterministic."""
+    from paper_1809_01971_b200 import decomp
+    g = torch.Generator(device="cuda").manual_seed(a * 1000 + b)
+    Pa = torch.randn((a, R), dtype=torch.float64, device="cuda", generator=g)
+    Pb = torch.randn((b, R), dtype=torch.float64, device="cuda", generator=g)
+    if ymajor == "j":
+        Y = torch.randn((R, N), dtype=torch.float64, device="cuda", generator=g)
+    else:
+        Y = torch.randn((N, R), dtype=torch.float64, device="cuda", generator=g).T  # unit stride along r
+    got = decomp._kr_contract(Pa, Pb, Y)
+    K = (Pa[:, None, :] * Pb[None, :, :]).reshape(a * b, R)
+    want = K @ Y
+    assert got.shape == want.shape
+    scale = float(torch.linalg.matrix_norm(K)) * float(torch.linalg.matrix_norm(Y)) / max(R, 1) ** 0.5
+    assert float((got - want).abs().max()) <= 1e-13 * max(scale, 1e-300) * max(R, 1) ** 0.5
+    assert torch.equal(decomp._kr_contract(Pa, Pb, Y), got)
+
+
 def test_left_sv_routes_agree(monkeypatch):
     """_left_sv through QR + the small Jacobi kernel (enabled up to 128 here;
     the product keeps it to 64) spans the same leading subspace as the
