@@ -70,3 +70,26 @@ def test_large_grid_route_matches_reference_route(i):
     assert abs(rep_big.iterations - rep_ref.iterations) <= 1
     assert e_big <= 2.0 * e_ref + 1e-6
     assert e_ab <= 2.0 * (e_big + e_ref)
+
+
+def test_pcg_stall_guard_stops_unconverged():
+    """pcg(..., stall=(window, factor)): the large-grid route's guard against
+    stagnating solves.  With a factor no residual history can satisfy, the
+    solve stops right after window + 1 iterations, unconverged, with its
+    residuals reported; without the option (the reference's signature) the
+    same solve converges."""
+    from paper_1809_01971_b200 import solver
+    n = 31
+    spec = fl.laplacian_spectrum(n, 3)
+    y, cfg = batch.problem(0, n)
+    kind = fl.CoreFunctionKind("g2", cfg.alpha, coeff_minus=cfg.beta, coeff_plus=cfg.gamma / cfg.beta)
+    fun = fl.LowRankOperator(fl.build_core(kind, spec, fl.TruncationSpec(tolerance=cfg.eps)))
+    pre = fl.build_preconditioner(kind, spec, cfg.precond_rank)
+    u, rep = solver.pcg(fun, pre, y, None, cfg)
+    assert rep.converged and rep.iterations >= 4
+    u2, rep2 = solver.pcg(fun, pre, y, None, cfg, stall=(2, 1e-12))
+    assert not rep2.converged and rep2.iterations == 3
+    assert len(rep2.residuals) == 4 and rep2.residuals[:4] == pytest.approx(rep.residuals[:4], rel=1e-6)
+    # the batch's own setting does not trip on a converging solve
+    u3, rep3 = solver.pcg(fun, pre, y, None, cfg, stall=batch._STALL)
+    assert rep3.converged and rep3.iterations == rep.iterations
