@@ -124,4 +124,11 @@ def ptr_arr(tensors):
 
 
 def call(name, *args):
-    check(getattr(load(), name)(*args))
+    fn = getattr(load(), name)
+    rc = fn(*args)
+    if rc == FL_ENOMEM:
+        # the library's stream-ordered scratch and torch's caching allocator
+        # share the device: hand torch's cached blocks back and retry once
+        torch.cuda.empty_cache()
+        rc = fn(*args)
+    check(rc)

@@ -17,7 +17,8 @@ void set_error(const char* fmt, ...);
     if (_e != cudaSuccess) {                                                  \
       ::fl::set_error("%s:%d: %s: %s", __FILE__, __LINE__, #expr,             \
                       cudaGetErrorString(_e));                                \
-      return FL_ECUDA;                                                        \
+      (void)cudaGetLastError(); /* reset the thread's (non-sticky) error */   \
+      return _e == cudaErrorMemoryAllocation ? FL_ENOMEM : FL_ECUDA;          \
     }                                                                         \
   } while (0)
 
