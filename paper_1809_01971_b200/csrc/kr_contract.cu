@@ -59,39 +59,50 @@ __global__ void __launch_bounds__(KNT) k_kr_dmma(const KrArgs g) {
   // A tile element e = t + KNT * r: kk = e & 15 (reduction index, unit
   // stride in Pa / Pb), mm = e >> 4: rows (t >> 4) + 8 r of the tile
   const int akk = t & (KBK - 1);
-  int rowa[8], rowb[8];  // Pa / Pb rows of this thread's tile rows (-1: past the end)
+  // per-thread operand pointers, advanced by one K tile per load (address
+  // arithmetic was a third of the instructions with per-load index products)
+  const double* pa[8];
+  const double* pb[8];
+  const double* py[8];
+  unsigned okrow = 0, okcol = 0;
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     const int64_t gm = m0 + (t >> 4) + 8 * r;
+    pa[r] = g.Pa;
+    pb[r] = g.Pb;
     if (gm < M) {
       const int64_t ia = gm / g.b;
-      rowa[r] = (int)ia;
-      rowb[r] = (int)(gm - ia * g.b);
-    } else {
-      rowa[r] = rowb[r] = -1;
+      pa[r] = g.Pa + ia * g.R + k_lo + akk;
+      pb[r] = g.Pb + (gm - ia * g.b) * g.R + k_lo + akk;
+      okrow |= 1u << r;
+    }
+    const int e = t + KNT * r;
+    const int kb = Y_JMAJOR ? (e >> 6) : (e & (KBK - 1));
+    const int nn = Y_JMAJOR ? (e & (KBN - 1)) : (e >> 4);
+    py[r] = g.Y;
+    if (n0 + nn < g.N) {
+      py[r] = g.Y + (k_lo + kb) * g.sYr + (n0 + nn) * g.sYj;
+      okcol |= 1u << r;
     }
   }
+  const int64_t ystep = (int64_t)KBK * g.sYr;
   // raw Pa and Pb values: the product is formed at store time so that the
   // loads stay in flight during the MMAs of the current tile
   double ra[8], rp[8], rb[8];
   auto load_tile = [&](int64_t k0) {
-    const int64_t gk = k0 + akk;
+    const int64_t krem = k_hi - k0;  // reduction indices left in this split
+    const bool aok = akk < krem;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
-      const bool ok = rowa[r] >= 0 && gk < k_hi;
-      ra[r] = ok ? __ldg(g.Pa + rowa[r] * g.R + gk) : 0.0;
-      rp[r] = ok ? __ldg(g.Pb + rowb[r] * g.R + gk) : 0.0;
+      const bool ok = aok && ((okrow >> r) & 1u);
+      ra[r] = ok ? __ldg(pa[r]) : 0.0;
+      rp[r] = ok ? __ldg(pb[r]) : 0.0;
+      pa[r] += KBK;
+      pb[r] += KBK;
       const int e = t + KNT * r;
-      int kb, nn;
-      if (Y_JMAJOR) {
-        nn = e & (KBN - 1);
-        kb = e >> 6;
-      } else {
-        kb = e & (KBK - 1);
-        nn = e >> 4;
-      }
-      const int64_t gn = n0 + nn, gkb = k0 + kb;
-      rb[r] = (gn < g.N && gkb < k_hi) ? __ldg(g.Y + gkb * g.sYr + gn * g.sYj) : 0.0;
+      const int kb = Y_JMAJOR ? (e >> 6) : (e & (KBK - 1));
+      rb[r] = (kb < krem && ((okcol >> r) & 1u)) ? __ldg(py[r]) : 0.0;
+      py[r] += ystep;
     }
   };
   auto store_tile = [&]() {

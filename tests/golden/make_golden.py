@@ -175,8 +175,11 @@ def config1_alpha_cases():
     """BASELINE configs[1] at reduced n: 3D canonical control solves for every
     alpha the config names (0.25, 0.5, 0.75), beta=1e-2, rank-8 bump target,
     eps=1e-8, residual tol 1e-6 (reference solver.py:203-216).  n=15 and 31
-    finish in minutes on the reference; n=127 needs a 128 GiB all-pairs merge
-    matrix in the reference and is out of its reach.  One file per (n, alpha)
+    finish in minutes on the reference; n=63 was attempted (C1_SIZES=63
+    C1_ALPHAS=0.5, round 2): the reference process died with SIGSEGV after
+    ~25 minutes in this container (its all-pairs cosine matrices outgrow the
+    host memory), and n=127 needs a 128 GiB all-pairs merge matrix: both are
+    out of the reference's reach here.  One file per (n, alpha)
     so that cases can be generated in parallel processes."""
     sizes = [int(v) for v in os.environ.get("C1_SIZES", "15,31").split(",")]
     alphas = [float(v) for v in os.environ.get("C1_ALPHAS", "0.25,0.5,0.75").split(",")]
