@@ -25,7 +25,7 @@ def bucket(v, q=16):
     return (int(v) + q - 1) // q * q
 
 
-wrap(decomp, "_left_sv", lambda M, r: ("left_sv", bucket(min(M.shape)), bucket(max(M.shape), 512), "wide" if M.shape[0] <= M.shape[1] else "tall"))
+wrap(decomp, "_left_sv", lambda M, r, *a: ("left_sv", bucket(min(M.shape)), bucket(max(M.shape), 512), "wide" if M.shape[0] <= M.shape[1] else "tall"))
 wrap(decomp, "_svdvals", lambda M: ("svdvals", bucket(min(M.shape)), bucket(max(M.shape), 512)))
 wrap(decomp, "_svd", lambda M, compute_uv=True: ("lib_svd", bucket(min(M.shape)), bucket(max(M.shape), 512)))
 wrap(decomp, "_range_basis_gen", lambda block, n, R, w, *a, **k: ("range", n, bucket(R, 4096)))
