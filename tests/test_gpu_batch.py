@@ -82,6 +82,10 @@ def test_pcg_stall_guard_stops_unconverged():
     n = 31
     spec = fl.laplacian_spectrum(n, 3)
     y, cfg = batch.problem(0, n)
+    # tolerance 1e-7: the second residual (1.3e-5, measured) stays well above
+    # the guard's "within 10x of the tolerance" exemption
+    cfg = fl.SolverConfig(alpha=cfg.alpha, beta=cfg.beta, eps=cfg.eps, precond_rank=cfg.precond_rank,
+                          residual_tol=1e-7, k_max=cfg.k_max)
     kind = fl.CoreFunctionKind("g2", cfg.alpha, coeff_minus=cfg.beta, coeff_plus=cfg.gamma / cfg.beta)
     fun = fl.LowRankOperator(fl.build_core(kind, spec, fl.TruncationSpec(tolerance=cfg.eps)))
     pre = fl.build_preconditioner(kind, spec, cfg.precond_rank)
