@@ -31,7 +31,7 @@ constexpr int TS_CHUNK = 128;  // rows absorbed per phase
 // Shared-memory traffic per step is the reflector only; the chunk is never
 // written back.
 template <int LPC>
-__device__ __forceinline__ void absorb_chunk(double* Rs, int ldr, double* vbuf, double* sc, int k,
+__device__ __forceinline__ void absorb_chunk(double* Rs, int ldr, double* vbuf, double* sc, int k, bool tri,
                                              double (&x)[TS_CHUNK / LPC]) {
   constexpr int RPT = TS_CHUNK / LPC;
   const int c = threadIdx.x / LPC, q = threadIdx.x % LPC;
@@ -75,6 +75,7 @@ __device__ __forceinline__ void absorb_chunk(double* Rs, int ldr, double* vbuf, 
       double d0 = 0.0, d1 = 0.0;
 #pragma unroll
       for (int i0 = 0; i0 < RPT; i0 += 8) {
+        if (tri && LPC * i0 > j) break;  // merge: the reflector is zero below chunk row j
         double v[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = vb[q + LPC * (i0 + i)];
@@ -91,6 +92,7 @@ __device__ __forceinline__ void absorb_chunk(double* Rs, int ldr, double* vbuf, 
       d = fma(v0, rjc, d) * beta;
 #pragma unroll
       for (int i0 = 0; i0 < RPT; i0 += 8) {
+        if (tri && LPC * i0 > j) break;  // merge: the reflector is zero below chunk row j
         double v[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = vb[q + LPC * (i0 + i)];
@@ -139,7 +141,7 @@ __device__ __forceinline__ void tsqr_cta(const TsqrBatch& tb, int stride, double
         const long long col = pos + q + LPC * t;
         x[t] = (c < k && col < c_hi) ? M[c * rs + col * cs] : 0.0;
       }
-      absorb_chunk<LPC>(Rs, ldr, vbuf, sc, k, x);
+      absorb_chunk<LPC>(Rs, ldr, vbuf, sc, k, false, x);
     }
   } else {
     const int a = 2 * stride * g, b = a + stride;
@@ -154,7 +156,7 @@ __device__ __forceinline__ void tsqr_cta(const TsqrBatch& tb, int stride, double
       x[t] = (c < k && row < k && row <= c) ? Rb[(size_t)row * k + c] : 0.0;
     }
     __syncthreads();
-    absorb_chunk<LPC>(Rs, ldr, vbuf, sc, k, x);
+    absorb_chunk<LPC>(Rs, ldr, vbuf, sc, k, true, x);
   }
   __syncthreads();
   double* out = ts_slot(tb, i, slot);
