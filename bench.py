@@ -36,6 +36,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
+_T_START = time.perf_counter()
+
 METRIC = "operator-apply GDoF/s at d=3 (A^-alpha full format, n=511)"
 UNIT = "GDoF/s"
 ALPHA = 0.5
@@ -566,6 +568,17 @@ def run_batch(args, rank, world, dev):
     concs += [concs[-1]] * (len(ns) - len(concs))
     per_n = {}
     for n, count, conc in zip(ns, counts, concs):
+        # wall-time guard: the larger-n samples are skipped (and reported as
+        # such) once the whole bench has run longer than --time-budget seconds;
+        # every rank takes the same decision (rank 0's clock)
+        over = time.perf_counter() - _T_START > args.time_budget
+        if world > 1:
+            flag = torch.tensor([1.0 if over else 0.0], dtype=torch.float64, device=dev)
+            dist.broadcast(flag, src=0)
+            over = bool(flag.item() > 0.5)
+        if over and per_n:
+            per_n[str(n)] = {"problems": 0, "skipped": "bench time budget of %d s exceeded" % args.time_budget}
+            continue
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -606,6 +619,8 @@ def main(argv=None):
     p.add_argument("--batch-n", default="1023,2047,4095,8191")
     p.add_argument("--batch-count", default="64,2,2,2", help="problems per n (comma list, last repeats)")
     p.add_argument("--batch-conc", default="4,2,2,2", help="concurrent problems per GPU per n")
+    p.add_argument("--time-budget", type=int, default=480,
+                   help="skip the remaining configs[4] sizes once the run is older than this many seconds")
     args = p.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
