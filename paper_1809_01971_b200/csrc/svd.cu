@@ -210,16 +210,23 @@ __device__ __forceinline__ void jacobi_small_body(const double* __restrict__ Ab,
   if constexpr (PIV) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) perm[i] = i;
     __syncthreads();
-    double* cn = sig;  // column norms during the factorisation
+    // Partial column norms (squared) are DOWNDATED by the warp that updates
+    // the column (cn[c] -= R[j][c]^2, LAPACK dgeqp3's scheme) instead of
+    // being recomputed from the whole trailing block every step; a column
+    // whose norm has lost half its digits since its last exact evaluation
+    // (cn <= sqrt(eps) cn2) is re-evaluated by that warp on the spot.  They
+    // only choose the pivot: the reflector's norm is always the exact one.
+    double* cn = sig;
+    double* cn2 = reinterpret_cast<double*>(lastmod + n);  // norms at the last exact evaluation
+    for (int c = warp; c < n; c += nwarps) {
+      const double* wc = W + c * JS_LD;
+      double a = 0.0;
+      for (int i = lane; i < m; i += 32) a = fma(wc[i], wc[i], a);
+      a = warp_sum(a);
+      if (lane == 0) cn[c] = cn2[c] = a;
+    }
+    __syncthreads();
     for (int j = 0; j < n; ++j) {
-      for (int c = j + warp; c < n; c += nwarps) {
-        const double* wc = W + c * JS_LD;
-        double a = 0.0;
-        for (int i = j + lane; i < m; i += 32) a = fma(wc[i], wc[i], a);
-        a = warp_sum(a);
-        if (lane == 0) cn[c] = a;
-      }
-      __syncthreads();
       if (warp == 0) {
         double best = -1.0;
         int bi = j;
@@ -241,7 +248,6 @@ __device__ __forceinline__ void jacobi_small_body(const double* __restrict__ Ab,
       }
       __syncthreads();
       const int pc = flag[1];
-      const double xn2 = cn[pc];
       if (pc != j) {
         for (int i = threadIdx.x; i < m; i += blockDim.x) {
           const double t = W[j * JS_LD + i];
@@ -252,11 +258,18 @@ __device__ __forceinline__ void jacobi_small_body(const double* __restrict__ Ab,
           const int t = perm[j];
           perm[j] = perm[pc];
           perm[pc] = t;
+          // column j's own entries are not read again
+          cn[pc] = cn[j];
+          cn2[pc] = cn2[j];
         }
       }
       __syncthreads();
-      // Householder vector of column j (rows j..m-1): v = x - alpha e_j
+      // Householder vector of column j (rows j..m-1): v = x - alpha e_j; its
+      // norm exactly, by every warp (same data, same order: identical)
       double* wj = W + j * JS_LD;
+      double xn2 = 0.0;
+      for (int i = j + lane; i < m; i += 32) xn2 = fma(wj[i], wj[i], xn2);
+      xn2 = warp_sum(xn2);
       const double xj = wj[j];
       const double alpha = -copysign(sqrt(xn2), xj);
       const double vj = xj - alpha;
@@ -268,13 +281,29 @@ __device__ __forceinline__ void jacobi_small_body(const double* __restrict__ Ab,
           double d = 0.0;
           for (int i = j + lane; i < m; i += 32) d = fma(i == j ? vj : wj[i], wc[i], d);
           d = warp_sum(d) * beta;
-          for (int i = j + lane; i < m; i += 32) wc[i] = fma(-d, i == j ? vj : wj[i], wc[i]);
+          double rjc = 0.0;
+          for (int i = j + lane; i < m; i += 32) {
+            const double v = fma(-d, i == j ? vj : wj[i], wc[i]);
+            wc[i] = v;
+            if (i == j) rjc = v;  // lane 0: R[j][c]
+          }
+          rjc = __shfl_sync(0xffffffffu, rjc, 0);
+          const double t = cn[c] - rjc * rjc;
+          if (!(t > 1.5e-8 * cn2[c])) {
+            __syncwarp();
+            double a = 0.0;
+            for (int i = j + 1 + lane; i < m; i += 32) a = fma(wc[i], wc[i], a);
+            a = warp_sum(a);
+            if (lane == 0) cn[c] = cn2[c] = a;
+          } else if (lane == 0) {
+            cn[c] = t;
+          }
         }
       }
       __syncthreads();
       for (int i = j + threadIdx.x; i < m; i += blockDim.x) wj[i] = (i == j) ? (vtv > 0.0 ? alpha : xj) : 0.0;
-      __syncthreads();
     }
+    __syncthreads();
     // W := R^T (in place; R is upper triangular)
     for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
       const int c = idx / n, r = idx - c * n;
@@ -419,8 +448,9 @@ static int launch_jacobi_small(const double* A, int batch, int m, int n, double*
                                cudaStream_t st) {
   constexpr int LD = ROWS + 2;
   // W, sig (+1 for alignment), flag[4], perm[n], lastmod[n]
-  const size_t smem = sizeof(double) * ((size_t)n * LD + n + 1) + sizeof(int) * (4 + 2 * (size_t)n);
-  const size_t smem_max = sizeof(double) * ((size_t)JS_ROWS * LD + JS_ROWS + 1) + sizeof(int) * (4 + 2 * JS_ROWS);
+  // W, sig (+1 for alignment), flag[4], perm[n], lastmod[n], cn2[n] (PIV)
+  const size_t smem = sizeof(double) * ((size_t)n * LD + 2 * (size_t)n + 2) + sizeof(int) * (4 + 2 * (size_t)n);
+  const size_t smem_max = sizeof(double) * ((size_t)JS_ROWS * LD + 2 * JS_ROWS + 2) + sizeof(int) * (4 + 2 * JS_ROWS);
   static std::atomic<uint64_t> attr_js{0};
   int dev = 0;
   FL_CUDA_TRY(cudaGetDevice(&dev));
@@ -476,8 +506,8 @@ int left_sv_wide(int batch, const double* const* M, const int* k, const int64_t*
     jm.k[i] = k[i];
   }
   const int rows = kmax <= 32 ? 32 : kmax <= 64 ? 64 : kmax <= 96 ? 96 : 128;
-  const size_t smem = sizeof(double) * ((size_t)kmax * (rows + 2) + kmax + 1) + sizeof(int) * (4 + 2 * (size_t)kmax);
-  const size_t smem_max = sizeof(double) * ((size_t)JS_ROWS * (JS_ROWS + 2) + JS_ROWS + 1) + sizeof(int) * (4 + 2 * JS_ROWS);
+  const size_t smem = sizeof(double) * ((size_t)kmax * (rows + 2) + 2 * (size_t)kmax + 2) + sizeof(int) * (4 + 2 * (size_t)kmax);
+  const size_t smem_max = sizeof(double) * ((size_t)JS_ROWS * (JS_ROWS + 2) + 2 * JS_ROWS + 2) + sizeof(int) * (4 + 2 * JS_ROWS);
   static std::atomic<uint64_t> attr_jm{0};
   int dev = 0;
   FL_CUDA_TRY(cudaGetDevice(&dev));
