@@ -276,27 +276,45 @@ __device__ __forceinline__ void jacobi_small_body(const double* __restrict__ Ab,
       const double vtv = xn2 - xj * xj + vj * vj;
       if (vtv > 0.0) {
         const double beta = 2.0 / vtv;
-        for (int c = j + 1 + warp; c < n; c += nwarps) {
-          double* wc = W + c * JS_LD;
-          double d = 0.0;
-          for (int i = j + lane; i < m; i += 32) d = fma(i == j ? vj : wj[i], wc[i], d);
-          d = warp_sum(d) * beta;
-          double rjc = 0.0;
+        // four trailing columns per warp in flight (their reductions interleave)
+        for (int c0 = j + 1 + warp; c0 < n; c0 += 4 * nwarps) {
+          double d[4] = {0.0, 0.0, 0.0, 0.0};
           for (int i = j + lane; i < m; i += 32) {
-            const double v = fma(-d, i == j ? vj : wj[i], wc[i]);
-            wc[i] = v;
-            if (i == j) rjc = v;  // lane 0: R[j][c]
+            const double vi = i == j ? vj : wj[i];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int c = c0 + u * nwarps;
+              d[u] = fma(vi, W[(c < n ? c : j) * JS_LD + i], d[u]);
+            }
           }
-          rjc = __shfl_sync(0xffffffffu, rjc, 0);
-          const double t = cn[c] - rjc * rjc;
-          if (!(t > 1.5e-8 * cn2[c])) {
-            __syncwarp();
-            double a = 0.0;
-            for (int i = j + 1 + lane; i < m; i += 32) a = fma(wc[i], wc[i], a);
-            a = warp_sum(a);
-            if (lane == 0) cn[c] = cn2[c] = a;
-          } else if (lane == 0) {
-            cn[c] = t;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) d[u] += __shfl_xor_sync(0xffffffffu, d[u], o);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int c = c0 + u * nwarps;
+            if (c >= n) break;
+            double* wc = W + c * JS_LD;
+            const double du = d[u] * beta;
+            double rjc = 0.0;
+            for (int i = j + lane; i < m; i += 32) {
+              const double v = fma(-du, i == j ? vj : wj[i], wc[i]);
+              wc[i] = v;
+              if (i == j) rjc = v;  // lane 0: R[j][c]
+            }
+            rjc = __shfl_sync(0xffffffffu, rjc, 0);
+            const double t = cn[c] - rjc * rjc;
+            if (!(t > 1.5e-8 * cn2[c])) {
+              __syncwarp();
+              double a = 0.0;
+              for (int i = j + 1 + lane; i < m; i += 32) a = fma(wc[i], wc[i], a);
+              a = warp_sum(a);
+              if (lane == 0) cn[c] = cn2[c] = a;
+            } else if (lane == 0) {
+              cn[c] = t;
+            }
           }
         }
       }
